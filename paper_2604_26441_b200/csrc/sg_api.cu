@@ -1,0 +1,572 @@
+// extern "C" boundary (include/sg_api.h).  Every entry point catches C++
+// exceptions and CUDA errors and turns them into a nonzero status plus a
+// thread-local message; nothing throws across the ABI.
+#include <cstring>
+#include <mutex>
+#include "../../include/sg_api.h"
+#include "sg_hier.cuh"
+
+struct sg_fine {
+  sg::FineOp op;
+  sg::FineWork w;
+  std::mutex mu;
+};
+
+struct sg_hier {
+  sg_fine* fine = nullptr;
+  std::unique_ptr<sg::Hier> h;
+  std::mutex mu;
+};
+
+namespace {
+
+thread_local std::string g_err;
+
+template <class F>
+int guard(F&& f) {
+  try {
+    f();
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+  } catch (...) {
+    g_err = "unknown error";
+  }
+  return 1;
+}
+
+inline cudaStream_t S(void* p) { return reinterpret_cast<cudaStream_t>(p); }
+
+sg::Level& level_of(sg_hier* h, int level) {
+  SG_REQUIRE(level >= 0 && level < int(h->h->lv.size()), "level index out of range");
+  return *h->h->lv[size_t(level)];
+}
+
+// free-layout staging buffers for level-wise API calls
+struct Stage {
+  sg::DBuf<double> a, b;
+  sg::DBuf<float> fa, fb;
+  explicit Stage(int64_t nd) : a(static_cast<size_t>(nd)), b(static_cast<size_t>(nd)) {}
+};
+
+}  // namespace
+
+extern "C" {
+
+const char* sg_last_error(void) { return g_err.c_str(); }
+int sg_version(void) { return 1; }
+
+// ---------------------------------------------------------------- fine
+int sg_fine_create(int nx, int ny, int nz, const uint8_t* dof_mask, const double* E,
+                   const double* ke, sg_fine** out) {
+  return guard([&] {
+    SG_REQUIRE(out && E && ke, "null argument");
+    auto f = std::make_unique<sg_fine>();
+    cudaStream_t s = 0;
+    sg::build_grid(f->op.grid, nx, ny, nz, dof_mask, s);
+    const int64_t ne = f->op.grid.d.nelem();
+    std::vector<float> e32(static_cast<size_t>(ne));
+    double emax = -INFINITY;
+    for (int64_t e = 0; e < ne; ++e) {
+      e32[size_t(e)] = float(E[e]);
+      emax = E[e] > emax ? E[e] : emax;
+    }
+    f->op.emax = emax;
+    f->op.E64.alloc(size_t(ne));
+    f->op.E64.upload(E, size_t(ne), s);
+    f->op.E32.alloc(size_t(ne));
+    f->op.E32.upload(e32.data(), size_t(ne), s);
+    std::memcpy(f->op.ke_host, ke, sizeof(double) * 576);
+    for (int q = 0; q < 576; ++q) {
+      f->op.ke64.k[q] = ke[q];
+      f->op.ke32.k[q] = float(ke[q]);
+      f->op.ke16.k[q] = sg::bf16_round(float(ke[q]));
+    }
+    for (int q = 0; q < 24; ++q) f->op.kdiag.d[q] = ke[q * 24 + q];
+    const size_t nd = size_t(3 * f->op.grid.d.nnodes());
+    f->w.u64.alloc(nd);
+    f->w.y64.alloc(nd);
+    f->w.u32.alloc(nd);
+    f->w.y32.alloc(nd);
+    f->w.scal.alloc(8);
+    SG_CUDA(cudaStreamSynchronize(s));
+    *out = f.release();
+  });
+}
+
+void sg_fine_destroy(sg_fine* op) { delete op; }
+
+int64_t sg_fine_n_free(const sg_fine* op) { return op ? op->op.grid.n_free : -1; }
+
+int sg_fine_apply(sg_fine* f, int tag, const void* u, void* y, void* stream) {
+  return guard([&] {
+    std::lock_guard<std::mutex> lk(f->mu);
+    cudaStream_t s = S(stream);
+    if (tag == SG_TAG_FP64) {
+      sg::scatter_free<double>(f->op.grid, (const double*)u, f->w.u64.p, s);
+      sg::fine_apply_f64(f->op, f->w.u64.p, f->w.y64.p, s);
+      sg::gather_free<double>(f->op.grid, f->w.y64.p, (double*)y, s);
+    } else {
+      sg::scatter_free<float>(f->op.grid, (const float*)u, f->w.u32.p, s);
+      sg::fine_apply_tag(f->op, tag, f->w.u32.p, f->w.y32.p, s);
+      sg::gather_free<float>(f->op.grid, f->w.y32.p, (float*)y, s);
+    }
+  });
+}
+
+int sg_fine_diagonal(sg_fine* f, double* d, void* stream) {
+  return guard([&] {
+    std::lock_guard<std::mutex> lk(f->mu);
+    sg::fine_floored_diag(f->op, f->w, S(stream));
+    sg::gather_free<double>(f->op.grid, f->w.diag.p, d, S(stream));
+  });
+}
+
+int sg_fine_dense(sg_fine* f, double* K, void* stream) {
+  return guard([&] {
+    std::lock_guard<std::mutex> lk(f->mu);
+    cudaStream_t s = S(stream);
+    SG_REQUIRE(f->op.grid.n_free <= 20000, "dense assembly limited to 20000 free DOFs");
+    sg::DBuf<double> A(static_cast<size_t>(243 * f->op.grid.d.nnodes()));
+    sg::fine_to_stencil(f->op, A.p, s);
+    sg::stencil_to_dense(f->op.grid, A.p, K, 0.0, s);
+    SG_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+int sg_fine_boundary_codes(sg_fine* f, uint32_t* codes, int cap, int* n) {
+  return guard([&] {
+    std::lock_guard<std::mutex> lk(f->mu);
+    std::vector<uint32_t> c;
+    sg::boundary_codes(f->op, c, 0);
+    *n = int(c.size());
+    SG_REQUIRE(int(c.size()) <= cap, "boundary code buffer too small");
+    std::copy(c.begin(), c.end(), codes);
+  });
+}
+
+// ----------------------------------------------------------- hierarchy
+int sg_hier_create(sg_fine* f, const sg_hier_params* p, const double* triples,
+                   const uint32_t* codes, const double* diffs, int ncodes,
+                   const double* lam_cache, int n_cache, void* stream, sg_hier** out) {
+  return guard([&] {
+    std::lock_guard<std::mutex> lk(f->mu);
+    SG_REQUIRE(p && triples && out, "null argument");
+    sg::HParams hp;
+    hp.levels = p->levels;
+    hp.policy = p->policy;
+    hp.smoother_kind = p->smoother_kind;
+    hp.degree = p->degree;
+    hp.alpha = p->alpha;
+    hp.omega = p->omega;
+    hp.coarse_smooth_steps = p->coarse_smooth_steps;
+    hp.cholesky_cutoff = p->cholesky_cutoff;
+    hp.coarse_pcg_steps = p->coarse_pcg_steps;
+    hp.power_seed = p->power_seed;
+    sg::L1Tables t;
+    std::memcpy(t.tri, triples, sizeof(double) * 8 * 576);
+    t.codes.assign(codes, codes + ncodes);
+    t.diffs.assign(diffs, diffs + size_t(ncodes) * 576);
+    auto h = std::make_unique<sg_hier>();
+    h->fine = f;
+    h->h = sg::hier_build(&f->op, f->w, hp, t, lam_cache, n_cache, S(stream));
+    *out = h.release();
+  });
+}
+
+void sg_hier_destroy(sg_hier* h) { delete h; }
+
+int sg_hier_get_info(sg_hier* h, sg_hier_info* info) {
+  return guard([&] {
+    info->n_levels = int(h->h->lv.size());
+    info->clamped = h->h->clamped ? 1 : 0;
+    info->coarsest_dense = h->h->coarsest_mode == 0 ? 1 : 0;
+    info->eps = h->h->eps;
+  });
+}
+
+int sg_hier_level_info(sg_hier* h, int level, sg_level_info* info) {
+  return guard([&] {
+    std::lock_guard<std::mutex> lk(h->mu);
+    sg::Level& L = level_of(h, level);
+    info->nx = L.g->d.nx;
+    info->ny = L.g->d.ny;
+    info->nz = L.g->d.nz;
+    info->tag = L.tag;
+    info->n_free = L.g->n_free;
+    if (!L.is_fine && L.st.nnz == 0) L.st.nnz = sg::stencil_count_nnz(*L.g, L.st.A64.p, 0);
+    info->nnz = L.is_fine ? 0 : L.st.nnz;
+    info->lam_max = L.lam;
+  });
+}
+
+int sg_hier_level_csr(sg_hier* h, int level, int64_t* indptr, int64_t* indices, double* data) {
+  return guard([&] {
+    std::lock_guard<std::mutex> lk(h->mu);
+    sg::Level& L = level_of(h, level);
+    SG_REQUIRE(!L.is_fine, "level 0 is matrix-free");
+    sg::stencil_export_csr(*L.g, L.st.A64.p, indptr, indices, data, 0);
+  });
+}
+
+int sg_hier_level_mask(sg_hier* h, int level, uint8_t* mask) {
+  return guard([&] {
+    sg::Level& L = level_of(h, level);
+    const int64_t nn = L.g->d.nnodes();
+    for (int64_t n = 0; n < nn; ++n)
+      for (int a = 0; a < 3; ++a) mask[3 * n + a] = (L.g->h_nmask[size_t(n)] >> a) & 1;
+  });
+}
+
+int sg_hier_level_diag(sg_hier* h, int level, double* d, void* stream) {
+  return guard([&] {
+    std::lock_guard<std::mutex> lk(h->mu);
+    sg::Level& L = level_of(h, level);
+    sg::gather_free<double>(*L.g, L.diag.p, d, S(stream));
+  });
+}
+
+int sg_hier_cycle(sg_hier* h, int gamma, const double* r, double* z, void* stream) {
+  return guard([&] {
+    std::lock_guard<std::mutex> lk(h->mu);
+    cudaStream_t s = S(stream);
+    sg::Level& L0 = *h->h->lv[0];
+    sg::scatter_free<double>(*L0.g, r, L0.w.r.p, s);
+    sg::cycle(*h->h, 0, gamma, s);
+    sg::gather_free<double>(*L0.g, L0.w.x.p, z, s);
+  });
+}
+
+int sg_hier_level_apply(sg_hier* h, int level, int tag, const void* x, void* y, void* stream) {
+  return guard([&] {
+    std::lock_guard<std::mutex> lk(h->mu);
+    cudaStream_t s = S(stream);
+    sg::Level& L = level_of(h, level);
+    const int64_t nd = L.nd();
+    Stage st(nd);
+    if (tag == SG_TAG_FP64) {
+      sg::scatter_free<double>(*L.g, (const double*)x, st.a.p, s);
+      sg::level_apply(*h->h, L, tag, st.a.p, st.b.p, s);
+      sg::gather_free<double>(*L.g, st.b.p, (double*)y, s);
+    } else {
+      st.fa.alloc(size_t(nd));
+      st.fb.alloc(size_t(nd));
+      sg::scatter_free<float>(*L.g, (const float*)x, st.fa.p, s);
+      sg::level_apply(*h->h, L, tag, st.fa.p, st.fb.p, s);
+      sg::gather_free<float>(*L.g, st.fb.p, (float*)y, s);
+    }
+    SG_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+int sg_hier_level_smooth(sg_hier* h, int level, const double* b, const double* x0, double* out,
+                         void* stream) {
+  return guard([&] {
+    std::lock_guard<std::mutex> lk(h->mu);
+    cudaStream_t s = S(stream);
+    sg::Level& L = level_of(h, level);
+    const int64_t nd = L.nd();
+    Stage st(nd);
+    sg::DBuf<double> xo(static_cast<size_t>(nd));
+    sg::scatter_free<double>(*L.g, b, st.a.p, s);
+    if (x0) sg::scatter_free<double>(*L.g, x0, st.b.p, s);
+    sg::level_smooth(*h->h, level, st.a.p, x0 ? st.b.p : nullptr, xo.p, s);
+    sg::gather_free<double>(*L.g, xo.p, out, s);
+    SG_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+int sg_hier_prolong(sg_hier* h, int level, const double* xc, double* xf, void* stream) {
+  return guard([&] {
+    std::lock_guard<std::mutex> lk(h->mu);
+    cudaStream_t s = S(stream);
+    SG_REQUIRE(level + 1 < int(h->h->lv.size()), "no coarser level");
+    sg::Level& F = level_of(h, level);
+    sg::Level& C = level_of(h, level + 1);
+    sg::DBuf<double> a(static_cast<size_t>(C.nd())), b(static_cast<size_t>(F.nd()));
+    sg::scatter_free<double>(*C.g, xc, a.p, s);
+    sg::prolong(*F.g, *C.g, a.p, b.p, false, s);
+    sg::gather_free<double>(*F.g, b.p, xf, s);
+    SG_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+int sg_hier_restrict(sg_hier* h, int level, const double* xf, double* xc, void* stream) {
+  return guard([&] {
+    std::lock_guard<std::mutex> lk(h->mu);
+    cudaStream_t s = S(stream);
+    SG_REQUIRE(level + 1 < int(h->h->lv.size()), "no coarser level");
+    sg::Level& F = level_of(h, level);
+    sg::Level& C = level_of(h, level + 1);
+    sg::DBuf<double> a(static_cast<size_t>(F.nd())), b(static_cast<size_t>(C.nd()));
+    sg::scatter_free<double>(*F.g, xf, a.p, s);
+    sg::restrict_(*F.g, *C.g, a.p, b.p, s);
+    sg::gather_free<double>(*C.g, b.p, xc, s);
+    SG_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+int sg_hier_coarsest_solve(sg_hier* h, const double* r, double* x, void* stream) {
+  return guard([&] {
+    std::lock_guard<std::mutex> lk(h->mu);
+    cudaStream_t s = S(stream);
+    sg::Level& L = *h->h->lv.back();
+    sg::scatter_free<double>(*L.g, r, L.w.r.p, s);
+    sg::coarsest_solve(*h->h, L.w.r.p, L.w.x.p, s);
+    sg::gather_free<double>(*L.g, L.w.x.p, x, s);
+  });
+}
+
+int sg_hier_transfer_csr(sg_hier* h, int level, int64_t* indptr, int64_t* indices, double* data,
+                         int64_t* nnz) {
+  return guard([&] {
+    std::lock_guard<std::mutex> lk(h->mu);
+    SG_REQUIRE(level + 1 < int(h->h->lv.size()), "no coarser level");
+    sg::transfer_export_csr(*level_of(h, level).g, *level_of(h, level + 1).g, indptr, indices,
+                            data, nnz, 0);
+  });
+}
+
+// -------------------------------------------------------------- solvers
+static int run_solver(int which, sg_fine* f, int ktag, sg_hier* h, int gamma, const double* b,
+                      double* x, const sg_solver_cfg* cfg, sg_report* rep, double* history,
+                      void* stream) {
+  return guard([&] {
+    std::unique_lock<std::mutex> lf(f->mu);
+    std::unique_lock<std::mutex> lh;
+    if (h) {
+      SG_REQUIRE(h->fine == f, "hierarchy built for a different operator");
+      lh = std::unique_lock<std::mutex>(h->mu);
+    }
+    cudaStream_t s = S(stream);
+    sg::fine_floored_diag(f->op, f->w, s);
+    sg::NativeSys sys{&f->op, &f->w, ktag, h ? h->h.get() : nullptr, gamma};
+    sg::SolverCfg c{cfg->tol, cfg->maxiter, cfg->restart};
+    sg::SolveOut o;
+    std::vector<double> hist;
+    const int64_t nd = 3 * f->op.grid.d.nnodes();
+    sg::DBuf<double> bn(static_cast<size_t>(nd)), xn(static_cast<size_t>(nd));
+    sg::scatter_free<double>(f->op.grid, b, bn.p, s);
+    if (which == 0) sg::pcg_native(sys, bn.p, xn.p, c, o, hist, s);
+    else sg::fgmres_native(sys, bn.p, xn.p, c, o, hist, s);
+    sg::gather_free<double>(f->op.grid, xn.p, x, s);
+    SG_CUDA(cudaStreamSynchronize(s));
+    rep->converged = o.converged;
+    rep->iterations = o.iterations;
+    rep->final_true_residual = o.final_true_residual;
+    rep->failure_kind = o.failure_kind;
+    rep->wall_time = o.wall_time;
+    if (history) std::copy(hist.begin(), hist.end(), history);
+  });
+}
+
+int sg_pcg(sg_fine* f, int ktag, sg_hier* h, int gamma, const double* b, double* x,
+           const sg_solver_cfg* cfg, sg_report* rep, double* history, void* stream) {
+  return run_solver(0, f, ktag, h, gamma, b, x, cfg, rep, history, stream);
+}
+
+int sg_fgmres(sg_fine* f, int ktag, sg_hier* h, int gamma, const double* b, double* x,
+              const sg_solver_cfg* cfg, sg_report* rep, double* history, void* stream) {
+  return run_solver(1, f, ktag, h, gamma, b, x, cfg, rep, history, stream);
+}
+
+int sg_lanczos(sg_fine* f, sg_hier* h, int gamma, int m, uint64_t seed, double* H, int* used,
+               int* partial, void* stream) {
+  return guard([&] {
+    std::unique_lock<std::mutex> lf(f->mu);
+    std::unique_lock<std::mutex> lh(h->mu);
+    SG_REQUIRE(h->fine == f, "hierarchy built for a different operator");
+    sg::NativeSys sys{&f->op, &f->w, SG_TAG_FP64, h->h.get(), gamma};
+    std::vector<double> Hv;
+    int u = 0;
+    bool part = false;
+    sg::lanczos_native(sys, m, seed, Hv, u, part, S(stream));
+    std::copy(Hv.begin(), Hv.end(), H);
+    *used = u;
+    *partial = part ? 1 : 0;
+  });
+}
+
+}  // extern "C"
+
+// ------------------------------------------------------------ vectors
+namespace {
+
+template <class T>
+struct DotT {
+  const T* a;
+  const T* b;
+  __device__ void operator()(int64_t i, double (&acc)[1]) const {
+    acc[0] += double(a[i]) * double(b[i]);
+  }
+};
+
+template <class T> __device__ __forceinline__ T mulr(T a, T b);
+template <> __device__ __forceinline__ double mulr(double a, double b) { return __dmul_rn(a, b); }
+template <> __device__ __forceinline__ float mulr(float a, float b) { return __fmul_rn(a, b); }
+template <class T> __device__ __forceinline__ T addr(T a, T b);
+template <> __device__ __forceinline__ double addr(double a, double b) { return __dadd_rn(a, b); }
+template <> __device__ __forceinline__ float addr(float a, float b) { return __fadd_rn(a, b); }
+template <class T> __device__ __forceinline__ T subr(T a, T b);
+template <> __device__ __forceinline__ double subr(double a, double b) { return __dsub_rn(a, b); }
+template <> __device__ __forceinline__ float subr(float a, float b) { return __fsub_rn(a, b); }
+template <class T> __device__ __forceinline__ T divr(T a, T b);
+template <> __device__ __forceinline__ double divr(double a, double b) { return __ddiv_rn(a, b); }
+template <> __device__ __forceinline__ float divr(float a, float b) { return __fdiv_rn(a, b); }
+
+// op: 0 axpy (y = y + s*x), 1 xpby (y = x + s*y), 2 sub (c = a - b), 3 mul, 4 scale, 5 div
+template <class T>
+__global__ void vec_kernel(int op, int64_t n, const T* __restrict__ a, const T* __restrict__ b,
+                           T* __restrict__ c, T sc) {
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  switch (op) {
+    case 0: c[i] = addr(c[i], mulr(sc, a[i])); break;
+    case 1: c[i] = addr(a[i], mulr(sc, c[i])); break;
+    case 2: c[i] = subr(a[i], b[i]); break;
+    case 3: c[i] = mulr(a[i], b[i]); break;
+    case 4: c[i] = mulr(a[i], sc); break;
+    case 5: c[i] = divr(a[i], sc); break;
+  }
+}
+
+__global__ void bf16_kernel(int64_t n, const float* __restrict__ a, float* __restrict__ b) {
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) b[i] = sg::bf16_round(a[i]);
+}
+
+thread_local sg::RedWork t_red;
+thread_local sg::DBuf<double> t_scal;
+
+int vec_op(int dtype, int op, int64_t n, const void* a, const void* b, void* c, double sc,
+           void* stream) {
+  return guard([&] {
+    if (n <= 0) return;
+    const int nb = sg::grid_blocks(n, 256);
+    if (dtype == 0)
+      vec_kernel<double><<<nb, 256, 0, S(stream)>>>(op, n, (const double*)a, (const double*)b,
+                                                     (double*)c, sc);
+    else
+      vec_kernel<float><<<nb, 256, 0, S(stream)>>>(op, n, (const float*)a, (const float*)b,
+                                                    (float*)c, float(sc));
+    SG_CHECK_LAUNCH();
+  });
+}
+
+}  // namespace
+
+extern "C" {
+
+int sg_vec_dot(int dtype, int64_t n, const void* a, const void* b, double* out, void* stream) {
+  return guard([&] {
+    cudaStream_t s = S(stream);
+    if (!t_scal.p) t_scal.alloc(1);
+    if (n <= 0) {
+      *out = 0.0;
+      return;
+    }
+    if (dtype == 0)
+      sg::launch_reduce<1>(n, DotT<double>{(const double*)a, (const double*)b},
+                           sg::StoreTo<1>{{t_scal.p}}, t_red, s);
+    else
+      sg::launch_reduce<1>(n, DotT<float>{(const float*)a, (const float*)b},
+                           sg::StoreTo<1>{{t_scal.p}}, t_red, s);
+    SG_CUDA(cudaMemcpyAsync(out, t_scal.p, sizeof(double), cudaMemcpyDeviceToHost, s));
+    SG_CUDA(cudaStreamSynchronize(s));
+  });
+}
+int sg_vec_axpy(int dtype, int64_t n, double alpha, const void* x, void* y, void* stream) {
+  return vec_op(dtype, 0, n, x, nullptr, y, alpha, stream);
+}
+int sg_vec_xpby(int dtype, int64_t n, const void* x, double beta, void* y, void* stream) {
+  return vec_op(dtype, 1, n, x, nullptr, y, beta, stream);
+}
+int sg_vec_sub(int dtype, int64_t n, const void* a, const void* b, void* c, void* stream) {
+  return vec_op(dtype, 2, n, a, b, c, 0.0, stream);
+}
+int sg_vec_mul(int dtype, int64_t n, const void* a, const void* b, void* c, void* stream) {
+  return vec_op(dtype, 3, n, a, b, c, 0.0, stream);
+}
+int sg_vec_scale(int dtype, int64_t n, const void* a, double s, void* c, void* stream) {
+  return vec_op(dtype, 4, n, a, nullptr, c, s, stream);
+}
+int sg_vec_div(int dtype, int64_t n, const void* a, double s, void* c, void* stream) {
+  return vec_op(dtype, 5, n, a, nullptr, c, s, stream);
+}
+int sg_vec_bf16(int64_t n, const float* a, float* b, void* stream) {
+  return guard([&] {
+    if (n <= 0) return;
+    bf16_kernel<<<sg::grid_blocks(n, 256), 256, 0, S(stream)>>>(n, a, b);
+    SG_CHECK_LAUNCH();
+  });
+}
+
+}  // extern "C"
+
+// ------------------------------------------------- standalone transfers
+struct sg_transfer {
+  sg::Grid fine, coarse;
+};
+
+extern "C" {
+
+int sg_transfer_create(int nx, int ny, int nz, const uint8_t* mask, sg_transfer** out) {
+  return guard([&] {
+    auto t = std::make_unique<sg_transfer>();
+    sg::build_grid(t->fine, nx, ny, nz, mask, 0);
+    sg::build_coarse_grid(t->fine, t->coarse, 0);
+    *out = t.release();
+  });
+}
+
+void sg_transfer_destroy(sg_transfer* t) { delete t; }
+
+int sg_transfer_coarse_mask(sg_transfer* t, uint8_t* mask) {
+  return guard([&] {
+    const int64_t nn = t->coarse.d.nnodes();
+    for (int64_t n = 0; n < nn; ++n)
+      for (int a = 0; a < 3; ++a) mask[3 * n + a] = (t->coarse.h_nmask[size_t(n)] >> a) & 1;
+  });
+}
+
+int sg_transfer_apply(sg_transfer* t, int transpose, const double* x, double* y, void* stream) {
+  return guard([&] {
+    cudaStream_t s = S(stream);
+    sg::DBuf<double> a(static_cast<size_t>(3 * t->fine.d.nnodes())),
+        c(static_cast<size_t>(3 * t->coarse.d.nnodes()));
+    if (transpose) {
+      sg::scatter_free<double>(t->fine, x, a.p, s);
+      sg::restrict_(t->fine, t->coarse, a.p, c.p, s);
+      sg::gather_free<double>(t->coarse, c.p, y, s);
+    } else {
+      sg::scatter_free<double>(t->coarse, x, c.p, s);
+      sg::prolong(t->fine, t->coarse, c.p, a.p, false, s);
+      sg::gather_free<double>(t->fine, a.p, y, s);
+    }
+    SG_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+int sg_transfer_csr(sg_transfer* t, int64_t* indptr, int64_t* indices, double* data, int64_t* nnz) {
+  return guard([&] { sg::transfer_export_csr(t->fine, t->coarse, indptr, indices, data, nnz, 0); });
+}
+
+int sg_level1_csr(sg_fine* f, const double* triples, const uint32_t* codes, const double* diffs,
+                  int ncodes, int64_t* indptr, int64_t* indices, double* data, int64_t* nnz) {
+  return guard([&] {
+    std::lock_guard<std::mutex> lk(f->mu);
+    sg::Grid coarse;
+    sg::build_coarse_grid(f->op.grid, coarse, 0);
+    sg::L1Tables tb;
+    std::memcpy(tb.tri, triples, sizeof(double) * 8 * 576);
+    tb.codes.assign(codes, codes + ncodes);
+    tb.diffs.assign(diffs, diffs + size_t(ncodes) * 576);
+    sg::DBuf<double> A(static_cast<size_t>(243 * coarse.d.nnodes()));
+    sg::galerkin_level1(f->op, coarse, tb, A.p, 0);
+    const int64_t n = sg::stencil_count_nnz(coarse, A.p, 0);
+    *nnz = n;
+    if (indices) sg::stencil_export_csr(coarse, A.p, indptr, indices, data, 0);
+  });
+}
+
+}  // extern "C"

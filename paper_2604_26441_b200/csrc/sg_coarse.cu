@@ -1,0 +1,319 @@
+// Coarsest-level solvers (hierarchy.py:123-178).
+//
+//  * pcg80: the reference's fixed-count Jacobi-PCG on K + eps*I
+//    (_fixed_jacobi_pcg, hierarchy.py:139-162) as ONE persistent cooperative
+//    kernel: the 80 dependent steps never return to the host, dot products
+//    are reduced deterministically across the grid (fixed partial order),
+//    and the search-direction update is folded into the next SpMV (p is
+//    double-buffered and recomputed for neighbours on the fly) so each step
+//    costs two grid barriers instead of three.
+//  * dense: Cholesky of K + eps*I computed on device at setup, then the
+//    explicit inverse, so each V-cycle's coarsest solve is one GEMV.
+#include <cooperative_groups.h>
+#include <cmath>
+#include "sg_coarse.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace sg {
+
+struct Pcg80Args {
+  GridDesc g;
+  const double* A;     // stencil SoA (243 * nn)
+  const double* dinv;  // 1/(diag+eps), 0 on fixed
+  const double* b;
+  double* x;
+  double* r;
+  double* z;
+  double* p0;
+  double* p1;
+  double* q;
+  double* partials;  // 2 * gridDim.x
+  double eps;
+  int steps;
+};
+
+__device__ __forceinline__ double grid_total(const double* partials, int nb, double* sh) {
+  // every block sums the partials in index order: identical bits everywhere
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int b = 0; b < nb; ++b) s = __dadd_rn(s, ((volatile const double*)partials)[b]);
+    *sh = s;
+  }
+  __syncthreads();
+  return *sh;
+}
+
+__device__ __forceinline__ void block_partial(double v, double* out, double* sm) {
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) sm[warp] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = sm[0];
+    for (int w = 1; w < int(blockDim.x >> 5); ++w) s += sm[w];
+    *out = s;
+  }
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(256) pcg80_kernel(Pcg80Args P) {
+  cg::grid_group grid = cg::this_grid();
+  __shared__ double sm[8];
+  __shared__ double tot;
+  const int64_t nn = P.g.nnodes();
+  const int NX = P.g.nx + 1, NY = P.g.ny + 1;
+  const int64_t tid = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  const int nb = gridDim.x;
+  double* partA = P.partials;
+  double* partB = P.partials + nb;
+
+  // x = 0; r = b; z = dinv*r; p = z; rz = r.z
+  double loc = 0.0;
+  for (int64_t d = tid; d < 3 * nn; d += stride) {
+    const double rv = P.b[d];
+    const double zv = __dmul_rn(P.dinv[d], rv);
+    P.x[d] = 0.0;
+    P.r[d] = rv;
+    P.z[d] = zv;
+    P.p0[d] = zv;
+    loc += rv * zv;
+  }
+  block_partial(loc, &partB[blockIdx.x], sm);
+  grid.sync();
+  double rz = grid_total(partB, nb, &tot);
+  double beta = 0.0;
+  bool have_beta = false;
+  for (int s = 0; s < P.steps; ++s) {
+    const double* pold = (s & 1) ? P.p1 : P.p0;
+    double* pnew = (s & 1) ? P.p0 : P.p1;
+    // phase A: p_new = z + beta*p_old (on the fly), q = K p_new + eps p_new, pq
+    loc = 0.0;
+    for (int64_t node = tid; node < nn; node += stride) {
+      const int i = int(node % NX), j = int((node / NX) % NY), k = int(node / (int64_t(NX) * NY));
+      double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+      for (int dk = -1; dk <= 1; ++dk) {
+        if (k + dk < 0 || k + dk > P.g.nz) continue;
+        for (int dj = -1; dj <= 1; ++dj) {
+          if (j + dj < 0 || j + dj > P.g.ny) continue;
+          for (int di = -1; di <= 1; ++di) {
+            if (i + di < 0 || i + di > P.g.nx) continue;
+            const int slot = (dk + 1) * 9 + (dj + 1) * 3 + (di + 1);
+            const int64_t m = node + di + int64_t(NX) * (dj + int64_t(NY) * dk);
+            double pv[3];
+#pragma unroll
+            for (int c = 0; c < 3; ++c)
+              pv[c] = have_beta ? __dadd_rn(P.z[3 * m + c], __dmul_rn(beta, pold[3 * m + c]))
+                                : pold[3 * m + c];
+            const double* a = P.A + int64_t(slot) * 9 * nn + node;
+            s0 = __dadd_rn(s0, __dmul_rn(a[0 * nn], pv[0]));
+            s0 = __dadd_rn(s0, __dmul_rn(a[1 * nn], pv[1]));
+            s0 = __dadd_rn(s0, __dmul_rn(a[2 * nn], pv[2]));
+            s1 = __dadd_rn(s1, __dmul_rn(a[3 * nn], pv[0]));
+            s1 = __dadd_rn(s1, __dmul_rn(a[4 * nn], pv[1]));
+            s1 = __dadd_rn(s1, __dmul_rn(a[5 * nn], pv[2]));
+            s2 = __dadd_rn(s2, __dmul_rn(a[6 * nn], pv[0]));
+            s2 = __dadd_rn(s2, __dmul_rn(a[7 * nn], pv[1]));
+            s2 = __dadd_rn(s2, __dmul_rn(a[8 * nn], pv[2]));
+            if (slot == 13) {
+#pragma unroll
+              for (int c = 0; c < 3; ++c) pnew[3 * node + c] = pv[c];
+            }
+          }
+        }
+      }
+      const double sv[3] = {s0, s1, s2};
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        const double pc = pnew[3 * node + c];
+        const double qv = __dadd_rn(sv[c], __dmul_rn(P.eps, pc));
+        P.q[3 * node + c] = qv;
+        loc += pc * qv;
+      }
+    }
+    block_partial(loc, &partA[blockIdx.x], sm);
+    grid.sync();
+    const double pq = grid_total(partA, nb, &tot);
+    if (!(pq > 0.0) || !isfinite(pq)) break;
+    const double a = __ddiv_rn(rz, pq);
+    // phase B: x += a p; r -= a q; z = dinv r; rz_new
+    loc = 0.0;
+    for (int64_t d = tid; d < 3 * nn; d += stride) {
+      const double pv = pnew[d];
+      P.x[d] = __dadd_rn(P.x[d], __dmul_rn(a, pv));
+      const double rv = __dsub_rn(P.r[d], __dmul_rn(a, P.q[d]));
+      P.r[d] = rv;
+      const double zv = __dmul_rn(P.dinv[d], rv);
+      P.z[d] = zv;
+      loc += rv * zv;
+    }
+    block_partial(loc, &partB[blockIdx.x], sm);
+    grid.sync();
+    const double rzn = grid_total(partB, nb, &tot);
+    if (!(rzn > 0.0) || !isfinite(rzn)) break;
+    beta = __ddiv_rn(rzn, rz);
+    have_beta = true;
+    rz = rzn;
+  }
+}
+
+void Pcg80::setup(const Grid& g, const double* A, const double* diag, double eps_, int steps_,
+                  cudaStream_t s) {
+  grid = &g;
+  Aptr = A;
+  eps = eps_;
+  steps = steps_;
+  const int64_t nd = 3 * g.d.nnodes();
+  dinv.alloc(size_t(nd));
+  r.alloc(size_t(nd));
+  z.alloc(size_t(nd));
+  p0.alloc(size_t(nd));
+  p1.alloc(size_t(nd));
+  q.alloc(size_t(nd));
+  std::vector<double> h(static_cast<size_t>(size_t(nd)));
+  SG_CUDA(cudaMemcpyAsync(h.data(), diag, sizeof(double) * nd, cudaMemcpyDeviceToHost, s));
+  SG_CUDA(cudaStreamSynchronize(s));
+  std::vector<uint8_t> fixed(size_t(nd), 1);
+  std::vector<int32_t> f2d(static_cast<size_t>(size_t(g.n_free)));
+  SG_CUDA(cudaMemcpy(f2d.data(), g.free2dof.p, sizeof(int32_t) * g.n_free, cudaMemcpyDeviceToHost));
+  for (int32_t d : f2d) fixed[size_t(d)] = 0;
+  for (int64_t d = 0; d < nd; ++d) h[size_t(d)] = fixed[size_t(d)] ? 0.0 : 1.0 / (h[size_t(d)] + eps);
+  dinv.upload(h.data(), h.size(), s);
+  int dev = 0, nsm = 0, per_sm = 0;
+  SG_CUDA(cudaGetDevice(&dev));
+  SG_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+  SG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pcg80_kernel, 256, 0));
+  const int64_t want = (g.d.nnodes() + 255) / 256;
+  int64_t cap = int64_t(nsm) * std::max(per_sm, 1);
+  nblocks = int(std::max<int64_t>(1, std::min(want, cap)));
+  partials.alloc(size_t(2 * nblocks));
+  SG_CUDA(cudaStreamSynchronize(s));
+}
+
+void Pcg80::solve(const double* b, double* x, cudaStream_t s) {
+  Pcg80Args a;
+  a.g = grid->d;
+  a.A = Aptr;
+  a.dinv = dinv.p;
+  a.b = b;
+  a.x = x;
+  a.r = r.p;
+  a.z = z.p;
+  a.p0 = p0.p;
+  a.p1 = p1.p;
+  a.q = q.p;
+  a.partials = partials.p;
+  a.eps = eps;
+  a.steps = steps;
+  void* args[] = {&a};
+  SG_CUDA(cudaLaunchCooperativeKernel((void*)pcg80_kernel, dim3(nblocks), dim3(256), args, 0, s));
+}
+
+// ------------------------------------------------------------------ dense
+// Unblocked right-looking Cholesky of an n x n SPD matrix (row-major, lower
+// triangle used) by one 1024-thread CTA; returns info > 0 on a non-positive
+// pivot like LAPACK dpotrf.
+__global__ void __launch_bounds__(1024) chol_kernel(int n, double* L, int* info) {
+  __shared__ double piv;
+  __shared__ int bad;
+  if (threadIdx.x == 0) bad = 0;
+  __syncthreads();
+  for (int j = 0; j < n; ++j) {
+    if (threadIdx.x == 0) {
+      const double d = L[int64_t(j) * n + j];
+      if (!(d > 0.0) || !isfinite(d)) {
+        bad = j + 1;
+      } else {
+        piv = sqrt(d);
+        L[int64_t(j) * n + j] = piv;
+      }
+    }
+    __syncthreads();
+    if (bad) break;
+    for (int i = j + 1 + threadIdx.x; i < n; i += blockDim.x) L[int64_t(i) * n + j] /= piv;
+    __syncthreads();
+    // trailing update of the lower triangle: L[i][k] -= L[i][j] * L[k][j], k <= i
+    const int m = n - j - 1;
+    const int64_t tri = int64_t(m) * (m + 1) / 2;
+    for (int64_t t = threadIdx.x; t < tri; t += blockDim.x) {
+      // map t -> (ii, kk) with kk <= ii
+      int ii = int((sqrt(8.0 * double(t) + 1.0) - 1.0) * 0.5);
+      while (int64_t(ii) * (ii + 1) / 2 > t) --ii;
+      while (int64_t(ii + 1) * (ii + 2) / 2 <= t) ++ii;
+      const int kk = int(t - int64_t(ii) * (ii + 1) / 2);
+      const int i = j + 1 + ii, k = j + 1 + kk;
+      L[int64_t(i) * n + k] -= L[int64_t(i) * n + j] * L[int64_t(k) * n + j];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *info = bad;
+}
+
+// Column c of inv(L): forward substitution, one thread per column.
+__global__ void trinv_kernel(int n, const double* __restrict__ L, double* __restrict__ Y) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= n) return;
+  for (int i = 0; i < n; ++i) Y[int64_t(i) * n + c] = 0.0;
+  Y[int64_t(c) * n + c] = 1.0 / L[int64_t(c) * n + c];
+  for (int i = c + 1; i < n; ++i) {
+    double s = 0.0;
+    for (int t = c; t < i; ++t) s += L[int64_t(i) * n + t] * Y[int64_t(t) * n + c];
+    Y[int64_t(i) * n + c] = -s / L[int64_t(i) * n + i];
+  }
+}
+
+// Ainv[i][k] = sum_{t >= max(i,k)} Y[t][i] * Y[t][k]
+__global__ void ytY_kernel(int n, const double* __restrict__ Y, double* __restrict__ Ai) {
+  const int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (q >= int64_t(n) * n) return;
+  const int i = int(q / n), k = int(q % n);
+  double s = 0.0;
+  for (int t = i > k ? i : k; t < n; ++t) s += Y[int64_t(t) * n + i] * Y[int64_t(t) * n + k];
+  Ai[q] = s;
+}
+
+__global__ void gemv_node_kernel(int64_t nfree, const int32_t* __restrict__ f2d,
+                                 const double* __restrict__ Ai, const double* __restrict__ r,
+                                 double* __restrict__ x) {
+  // one warp per output row: x[f2d[row]] = sum_c Ai[row][c] * r[f2d[c]]
+  const int64_t row = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (row >= nfree) return;
+  const double* a = Ai + row * nfree;
+  double s = 0.0;
+  for (int64_t c = lane; c < nfree; c += 32) s += a[c] * r[f2d[c]];
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (lane == 0) x[f2d[row]] = s;
+}
+
+bool DenseInverse::setup(const Grid& g, const double* dense_with_eps, cudaStream_t s) {
+  grid = &g;
+  n = g.n_free;
+  SG_REQUIRE(n > 0 && n <= 20000, "dense coarsest size out of range");
+  DBuf<double> L(static_cast<size_t>(n * n)), Y(static_cast<size_t>(n * n));
+  SG_CUDA(cudaMemcpyAsync(L.p, dense_with_eps, sizeof(double) * n * n, cudaMemcpyDeviceToDevice, s));
+  DBuf<int> info(1);
+  chol_kernel<<<1, 1024, 0, s>>>(int(n), L.p, info.p);
+  SG_CHECK_LAUNCH();
+  int h_info = 0;
+  info.download(&h_info, 1, s);
+  SG_CUDA(cudaStreamSynchronize(s));
+  if (h_info) return false;  // LinAlgError -> pcg80 fallback (hierarchy.py:172-178)
+  trinv_kernel<<<grid_blocks(n, 64), 64, 0, s>>>(int(n), L.p, Y.p);
+  SG_CHECK_LAUNCH();
+  Ainv.alloc(size_t(n * n));
+  ytY_kernel<<<grid_blocks(n * n, 256), 256, 0, s>>>(int(n), Y.p, Ainv.p);
+  SG_CHECK_LAUNCH();
+  SG_CUDA(cudaStreamSynchronize(s));
+  return true;
+}
+
+void DenseInverse::solve(const double* r, double* x, cudaStream_t s) {
+  SG_CUDA(cudaMemsetAsync(x, 0, sizeof(double) * 3 * grid->d.nnodes(), s));
+  gemv_node_kernel<<<grid_blocks(n * 32, 256), 256, 0, s>>>(n, grid->free2dof.p, Ainv.p, r, x);
+  SG_CHECK_LAUNCH();
+}
+
+}  // namespace sg

@@ -1,0 +1,29 @@
+#pragma once
+#include "sg_kernels.cuh"
+
+namespace sg {
+
+// Fixed-count Jacobi-PCG on K + eps I (hierarchy.py:139-162), one
+// persistent cooperative launch per solve.
+struct Pcg80 {
+  const Grid* grid = nullptr;
+  const double* Aptr = nullptr;
+  double eps = 0.0;
+  int steps = 80;
+  int nblocks = 0;
+  DBuf<double> dinv, r, z, p0, p1, q, partials;
+  void setup(const Grid& g, const double* A, const double* diag, double eps, int steps,
+             cudaStream_t s);
+  void solve(const double* b, double* x, cudaStream_t s);
+};
+
+// Dense (K + eps I)^-1 from an on-device Cholesky (hierarchy.py:165-178).
+struct DenseInverse {
+  const Grid* grid = nullptr;
+  int64_t n = 0;
+  DBuf<double> Ainv;  // n x n, free ordering
+  bool setup(const Grid& g, const double* dense_with_eps, cudaStream_t s);
+  void solve(const double* r, double* x, cudaStream_t s);
+};
+
+}  // namespace sg

@@ -1,0 +1,425 @@
+// Hierarchy build and V/W-cycle (hierarchy.py:181-282), smoothers
+// (smoothers.py:67-152), all device-resident.
+//
+// Rounding points mirror the reference: the smoother of a
+// reduced-precision level runs its recurrence in FP32 with the coefficients
+// rounded to FP32 (wt(1/sigma), wt(a), wt(a*c)); the residual handed to the
+// coarse level is r64 - f64(K_tag x); transfers and coarse corrections are
+// FP64.  Elementwise updates use explicit round-to-nearest intrinsics so no
+// FMA contraction changes the numpy-equivalent bits.
+#include <cmath>
+#include "sg_hier.cuh"
+
+namespace sg {
+
+template <class T> __device__ __forceinline__ T fmul(T a, T b);
+template <> __device__ __forceinline__ double fmul<double>(double a, double b) { return __dmul_rn(a, b); }
+template <> __device__ __forceinline__ float fmul<float>(float a, float b) { return __fmul_rn(a, b); }
+template <class T> __device__ __forceinline__ T fadd(T a, T b);
+template <> __device__ __forceinline__ double fadd<double>(double a, double b) { return __dadd_rn(a, b); }
+template <> __device__ __forceinline__ float fadd<float>(float a, float b) { return __fadd_rn(a, b); }
+template <class T> __device__ __forceinline__ T fsub(T a, T b);
+template <> __device__ __forceinline__ double fsub<double>(double a, double b) { return __dsub_rn(a, b); }
+template <> __device__ __forceinline__ float fsub<float>(float a, float b) { return __fsub_rn(a, b); }
+
+#define SG_ELEMWISE(n) \
+  const int64_t i_ = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; \
+  if (i_ >= (n)) return;
+
+// ---------------------------------------------------------- smoother kernels
+// d = c0*(dinv*b); x = 0 + d   (chebyshev_smooth x0=None, smoothers.py:277-283)
+template <class T>
+__global__ void cheb_first0_kernel(int64_t n, const T* __restrict__ dinv, const T* __restrict__ b,
+                                   T c0, T* __restrict__ d, T* __restrict__ x) {
+  SG_ELEMWISE(n);
+  const T dv = fmul(c0, fmul(dinv[i_], b[i_]));
+  d[i_] = dv;
+  x[i_] = fadd(T(0), dv);
+}
+// r = b - y; d = c0*(dinv*r); x = x + d
+template <class T>
+__global__ void cheb_first_kernel(int64_t n, const T* __restrict__ dinv, const T* __restrict__ b,
+                                  const T* __restrict__ y, T c0, T* __restrict__ d, T* __restrict__ x) {
+  SG_ELEMWISE(n);
+  const T r = fsub(b[i_], y[i_]);
+  const T dv = fmul(c0, fmul(dinv[i_], r));
+  d[i_] = dv;
+  x[i_] = fadd(x[i_], dv);
+}
+// r = b - y; d = A*(dinv*r) + AC*d; x = x + d   (smoothers.py:104-108)
+template <class T>
+__global__ void cheb_step_kernel(int64_t n, const T* __restrict__ dinv, const T* __restrict__ b,
+                                 const T* __restrict__ y, T A, T AC, T* __restrict__ d, T* __restrict__ x) {
+  SG_ELEMWISE(n);
+  const T r = fsub(b[i_], y[i_]);
+  const T dv = fadd(fmul(A, fmul(dinv[i_], r)), fmul(AC, d[i_]));
+  d[i_] = dv;
+  x[i_] = fadd(x[i_], dv);
+}
+// x = w*(dinv*b)   (jacobi_smooth x0=None)
+template <class T>
+__global__ void jac_first0_kernel(int64_t n, const T* __restrict__ dinv, const T* __restrict__ b, T w,
+                                  T* __restrict__ x) {
+  SG_ELEMWISE(n);
+  x[i_] = fmul(w, fmul(dinv[i_], b[i_]));
+}
+// x = x + w*(dinv*(b - y))
+template <class T>
+__global__ void jac_step_kernel(int64_t n, const T* __restrict__ dinv, const T* __restrict__ b,
+                                const T* __restrict__ y, T w, T* __restrict__ x) {
+  SG_ELEMWISE(n);
+  x[i_] = fadd(x[i_], fmul(w, fmul(dinv[i_], fsub(b[i_], y[i_]))));
+}
+// d64 = r - f64(y)
+template <class T>
+__global__ void residual_kernel(int64_t n, const double* __restrict__ r, const T* __restrict__ y,
+                                double* __restrict__ d) {
+  SG_ELEMWISE(n);
+  d[i_] = __dsub_rn(r[i_], double(y[i_]));
+}
+__global__ void copy_kernel(int64_t n, const double* __restrict__ a, double* __restrict__ b) {
+  SG_ELEMWISE(n);
+  b[i_] = a[i_];
+}
+__global__ void recip_kernel(int64_t n, const double* __restrict__ d, double* __restrict__ di,
+                             float* __restrict__ di32) {
+  SG_ELEMWISE(n);
+  const double v = d[i_] != 0.0 ? __drcp_rn(d[i_]) : 0.0;
+  di[i_] = v;
+  di32[i_] = __double2float_rn(v);
+}
+
+template <class K>
+static void launch_ew(int64_t n, cudaStream_t s, K kernel_launch) {
+  kernel_launch(grid_blocks(n, 256), 256);
+  SG_CHECK_LAUNCH();
+}
+
+// ---------------------------------------------------------------- applies
+void fine_apply_tag(const FineOp& op, int tag, const void* x, void* y, cudaStream_t s) {
+  switch (tag) {
+    case TAG_FP64: fine_apply_f64(op, (const double*)x, (double*)y, s); break;
+    case TAG_FP32: fine_apply_f32(op, (const float*)x, (float*)y, s); break;
+    case TAG_BF16: fine_apply_bf16(op, (const float*)x, (float*)y, s); break;
+    default: throw Error("bad precision tag");
+  }
+}
+
+void level_apply(Hier& H, Level& L, int tag, const void* x, void* y, cudaStream_t s) {
+  if (L.is_fine) {
+    fine_apply_tag(*H.fine, tag, x, y, s);
+    return;
+  }
+  if (tag == TAG_FP64) {
+    stencil_apply<double>(*L.g, L.st.A64.p, (const double*)x, (double*)y, s);
+  } else if (tag == TAG_FP32) {
+    SG_REQUIRE(L.st.A32.p, "fp32 operator copy missing");
+    stencil_apply<float>(*L.g, L.st.A32.p, (const float*)x, (float*)y, s);
+  } else {
+    throw Error("bf16 tag on an assembled level is not produced by any policy");
+  }
+}
+
+// Working-type dispatch for the smoother.
+template <class T>
+struct WT;
+template <>
+struct WT<double> {
+  static double* x(Level& L) { return L.w.x.p; }
+  static double* y(Level& L) { return L.w.y64.p; }
+  static double* d(Level& L) { return L.w.dd64.p; }
+  static const double* dinv(Level& L) { return L.dinv.p; }
+};
+template <>
+struct WT<float> {
+  static float* x(Level& L) { return L.w.x32.p; }
+  static float* y(Level& L) { return L.w.y32.p; }
+  static float* d(Level& L) { return L.w.dd32.p; }
+  static const float* dinv(Level& L) { return L.dinv32.p; }
+};
+
+template <class T>
+static void smooth_t(Hier& H, Level& L, const T* b, const double* x0, double* out, cudaStream_t s) {
+  const int64_t n = L.nd();
+  T* x = WT<T>::x(L);
+  T* y = WT<T>::y(L);
+  T* d = WT<T>::d(L);
+  const T* dinv = WT<T>::dinv(L);
+  auto to_w = [&](const double* src) {
+    if constexpr (sizeof(T) == 8) {
+      if (src != (const double*)x) launch_ew(n, s, [&](int nb, int nt) { copy_kernel<<<nb, nt, 0, s>>>(n, src, (double*)x); });
+    } else {
+      cvt_f64_to_f32(n, src, (float*)x, s);
+    }
+  };
+  if (L.kind == 0) {  // Chebyshev (smoothers.py:67-110)
+    const double lam = L.lam;
+    const double sigma = 0.5 * (lam + L.alpha * lam);
+    const double delta = 0.5 * (lam - L.alpha * lam);
+    const T c0 = T(1.0 / sigma);
+    if (!x0) {
+      launch_ew(n, s, [&](int nb, int nt) { cheb_first0_kernel<T><<<nb, nt, 0, s>>>(n, dinv, b, c0, d, x); });
+    } else {
+      to_w(x0);
+      level_apply(H, L, L.tag, x, y, s);
+      launch_ew(n, s, [&](int nb, int nt) { cheb_first_kernel<T><<<nb, nt, 0, s>>>(n, dinv, b, y, c0, d, x); });
+    }
+    double a = 2.0 / sigma;
+    for (int it = 1; it < L.degree; ++it) {
+      level_apply(H, L, L.tag, x, y, s);
+      const double c = delta * delta * a / 4.0;
+      a = 1.0 / (sigma - c);
+      const T A = T(a), AC = T(a * c);
+      launch_ew(n, s, [&](int nb, int nt) { cheb_step_kernel<T><<<nb, nt, 0, s>>>(n, dinv, b, y, A, AC, d, x); });
+    }
+  } else {  // damped Jacobi (smoothers.py:113-131)
+    const T w = T(L.omega);
+    int steps = L.degree;
+    if (!x0) {
+      launch_ew(n, s, [&](int nb, int nt) { jac_first0_kernel<T><<<nb, nt, 0, s>>>(n, dinv, b, w, x); });
+      steps -= 1;
+    } else {
+      to_w(x0);
+    }
+    for (int it = 0; it < steps; ++it) {
+      level_apply(H, L, L.tag, x, y, s);
+      launch_ew(n, s, [&](int nb, int nt) { jac_step_kernel<T><<<nb, nt, 0, s>>>(n, dinv, b, y, w, x); });
+    }
+  }
+  if constexpr (sizeof(T) == 8) {
+    if (out != (double*)x) launch_ew(n, s, [&](int nb, int nt) { copy_kernel<<<nb, nt, 0, s>>>(n, (const double*)x, out); });
+  } else {
+    cvt_f32_to_f64(n, (const float*)x, out, s);
+  }
+}
+
+void level_smooth(Hier& H, int l, const double* b, const double* x0, double* out, cudaStream_t s) {
+  Level& L = *H.lv[size_t(l)];
+  if (L.tag == TAG_FP64) {
+    smooth_t<double>(H, L, b, x0, out, s);
+  } else {
+    cvt_f64_to_f32(L.nd(), b, L.w.b32.p, s);
+    smooth_t<float>(H, L, L.w.b32.p, x0, out, s);
+  }
+}
+
+void coarsest_solve(Hier& H, const double* r, double* x, cudaStream_t s) {
+  if (H.coarsest_mode == 0) H.dense.solve(r, x, s);
+  else H.pcg.solve(r, x, s);
+}
+
+// hierarchy.py:207-216
+void cycle(Hier& H, int l, int gamma, cudaStream_t s) {
+  Level& L = *H.lv[size_t(l)];
+  if (l == int(H.lv.size()) - 1) {
+    coarsest_solve(H, L.w.r.p, L.w.x.p, s);
+    return;
+  }
+  Level& C = *H.lv[size_t(l + 1)];
+  const int64_t n = L.nd();
+  // pre-smoothing writes x (f64) into w.d64 scratch first, then moved to w.x
+  double* x64 = L.w.d64.p;  // holds the f64 iterate across the coarse visits
+  level_smooth(H, l, L.w.r.p, nullptr, x64, s);
+  for (int g = 0; g < gamma; ++g) {
+    if (L.tag == TAG_FP64) {
+      level_apply(H, L, TAG_FP64, x64, L.w.y64.p, s);
+      launch_ew(n, s, [&](int nb, int nt) { residual_kernel<double><<<nb, nt, 0, s>>>(n, L.w.r.p, L.w.y64.p, L.w.x.p); });
+    } else {
+      cvt_f64_to_f32(n, x64, L.w.x32.p, s);
+      level_apply(H, L, L.tag, L.w.x32.p, L.w.y32.p, s);
+      launch_ew(n, s, [&](int nb, int nt) { residual_kernel<float><<<nb, nt, 0, s>>>(n, L.w.r.p, L.w.y32.p, L.w.x.p); });
+    }
+    restrict_(*L.g, *C.g, L.w.x.p, C.w.r.p, s);  // L.w.x used as residual scratch here
+    cycle(H, l + 1, gamma, s);
+    prolong(*L.g, *C.g, C.w.x.p, x64, /*add=*/true, s);
+  }
+  level_smooth(H, l, L.w.r.p, x64, L.w.x.p, s);
+}
+
+// ------------------------------------------------------- diag / power
+struct PowerRed {
+  const double* dinv;
+  double* w;
+  const double* v;
+  __device__ void operator()(int64_t i, double (&acc)[3]) const {
+    const double wv = __dmul_rn(dinv[i], w[i]);
+    w[i] = wv;
+    acc[0] += v[i] * wv;
+    acc[1] += v[i] * v[i];
+    acc[2] += wv * wv;
+  }
+};
+struct PowerPost {
+  double* sc;  // [0] lam, [1] stop, [2] ww
+  __device__ void operator()(const double (&t)[3]) const {
+    if (sc[1] != 0.0) return;
+    sc[0] = __ddiv_rn(t[0], t[1]);
+    sc[2] = t[2];
+  }
+};
+__global__ void power_norm_kernel(int64_t n, const double* __restrict__ w, double* __restrict__ v,
+                                  double* __restrict__ sc) {
+  SG_ELEMWISE(n);
+  if (sc[1] != 0.0) return;
+  const double nrm = sqrt(sc[2]);
+  if (nrm == 0.0) return;
+  v[i_] = __ddiv_rn(w[i_], nrm);
+}
+__global__ void power_stop_kernel(double* sc) {
+  if (sc[1] == 0.0 && sqrt(sc[2]) == 0.0) sc[1] = 1.0;
+}
+
+// estimate_lambda_max (smoothers.py:134-152) in FP64 on the level's own operator
+static double power_lambda(Hier& H, Level& L, int iters, uint64_t seed, cudaStream_t s) {
+  const int64_t n = L.nd();
+  double* v = L.w.r.p;
+  double* w = L.w.y64.p;
+  double* sc = H.scal.p;
+  SG_CUDA(cudaMemsetAsync(sc, 0, sizeof(double) * 4, s));
+  fill_gaussian_unit(*L.g, seed, v, H.red, sc + 3, s);
+  for (int it = 0; it < iters; ++it) {
+    level_apply(H, L, TAG_FP64, v, w, s);
+    launch_reduce<3>(n, PowerRed{L.dinv.p, w, v}, PowerPost{sc}, H.red, s);
+    launch_ew(n, s, [&](int nb, int nt) { power_norm_kernel<<<nb, nt, 0, s>>>(n, w, v, sc); });
+    power_stop_kernel<<<1, 1, 0, s>>>(sc);
+    SG_CHECK_LAUNCH();
+  }
+  double lam = 0.0;
+  SG_CUDA(cudaMemcpyAsync(&lam, sc, sizeof(double), cudaMemcpyDeviceToHost, s));
+  SG_CUDA(cudaStreamSynchronize(s));
+  return lam > 1e-6 ? lam : 1e-6;
+}
+
+void fine_floored_diag(FineOp& op, FineWork& w, cudaStream_t s) {
+  if (w.diag_ready) return;
+  w.diag.alloc(size_t(3 * op.grid.d.nnodes()));
+  fine_diag_raw(op, w.diag.p, s);
+  if (!w.scal.p) w.scal.alloc(8);
+  np_mean_free(op.grid, w.diag.p, w.scal.p, s);
+  diag_floor(op.grid, w.diag.p, w.scal.p, s);
+  const int64_t n = 3 * op.grid.d.nnodes();
+  w.dinv.alloc(size_t(n));
+  DBuf<float> junk(static_cast<size_t>(n));
+  launch_ew(n, s, [&](int nb, int nt) { recip_kernel<<<nb, nt, 0, s>>>(n, w.diag.p, w.dinv.p, junk.p); });
+  SG_CUDA(cudaStreamSynchronize(s));
+  w.diag_ready = true;
+}
+
+static void alloc_work(Level& L) {
+  const size_t n = size_t(L.nd());
+  L.w.r.alloc(n);
+  L.w.x.alloc(n);
+  L.w.d64.alloc(n);
+  L.w.y64.alloc(n);
+  L.w.dd64.alloc(n);
+  if (L.tag != TAG_FP64) {
+    L.w.b32.alloc(n);
+    L.w.x32.alloc(n);
+    L.w.y32.alloc(n);
+    L.w.dd32.alloc(n);
+  }
+}
+
+std::unique_ptr<Hier> hier_build(FineOp* fine, FineWork& fw, const HParams& p, const L1Tables& t,
+                                 const double* lam_cache, int n_cache, cudaStream_t s) {
+  SG_REQUIRE(p.levels >= 1, "need at least one level");
+  SG_REQUIRE(p.policy >= 0 && p.policy <= 2, "unknown precision policy");
+  auto H = std::make_unique<Hier>();
+  H->fine = fine;
+  H->policy = p.policy;
+  H->emax = fine->emax;
+  H->scal.alloc(16);
+  H->red.init(s);
+
+  // operators first (hierarchy.py:251-268)
+  {
+    auto L0 = std::make_unique<Level>();
+    L0->idx = 0;
+    L0->is_fine = true;
+    L0->g = &fine->grid;
+    H->lv.push_back(std::move(L0));
+  }
+  while (int(H->lv.size()) < p.levels) {
+    const Grid& cur = *H->lv.back()->g;
+    if (cur.d.nx % 2 || cur.d.ny % 2 || cur.d.nz % 2) {
+      H->clamped = true;
+      break;
+    }
+    auto C = std::make_unique<Level>();
+    C->idx = int(H->lv.size());
+    build_coarse_grid(cur, C->own, s);
+    if (C->own.n_free == 0) break;
+    C->g = &C->own;
+    const int64_t nn = C->own.d.nnodes();
+    C->st.A64.alloc(size_t(243 * nn));
+    if (H->lv.size() == 1) {
+      galerkin_level1(*fine, C->own, t, C->st.A64.p, s);
+    } else {
+      galerkin_next(cur, C->own, H->lv.back()->st.A64.p, C->st.A64.p, s);
+    }
+    H->lv.push_back(std::move(C));
+  }
+  const int nl = int(H->lv.size());
+  static const int pol[3][3] = {{TAG_FP64, TAG_FP64, TAG_FP64},
+                                {TAG_FP32, TAG_FP64, TAG_FP64},
+                                {TAG_BF16, TAG_FP32, TAG_FP64}};
+  for (int i = 0; i < nl; ++i) {
+    Level& L = *H->lv[size_t(i)];
+    L.tag = pol[p.policy][std::min(i, 2)];
+    L.kind = p.smoother_kind;
+    L.degree = i == 0 ? p.degree : p.coarse_smooth_steps;
+    L.alpha = p.alpha;
+    L.omega = p.omega;
+    const size_t n = size_t(L.nd());
+    L.diag.alloc(n);
+    L.dinv.alloc(n);
+    L.dinv32.alloc(n);
+    if (L.is_fine) {
+      fine_floored_diag(*fine, fw, s);
+      launch_ew(int64_t(n), s, [&](int nb, int nt) { copy_kernel<<<nb, nt, 0, s>>>(int64_t(n), fw.diag.p, L.diag.p); });
+    } else {
+      stencil_diag(*L.g, L.st.A64.p, L.diag.p, s);
+      np_mean_free(*L.g, L.diag.p, H->scal.p + 8, s);
+      diag_floor(*L.g, L.diag.p, H->scal.p + 8, s);
+      if (L.tag == TAG_FP32) {
+        L.st.A32.alloc(size_t(243 * L.g->d.nnodes()));
+        stencil_round_f32(*L.g, L.st.A64.p, L.st.A32.p, false, s);
+      }
+    }
+    launch_ew(int64_t(n), s, [&](int nb, int nt) { recip_kernel<<<nb, nt, 0, s>>>(int64_t(n), L.diag.p, L.dinv.p, L.dinv32.p); });
+    alloc_work(L);
+    if (lam_cache && i < n_cache) {
+      L.lam = lam_cache[i];
+    } else {
+      L.lam = 1.1 * power_lambda(*H, L, i == 0 ? 20 : 10, p.power_seed + uint64_t(i), s);
+    }
+  }
+
+  // coarsest (hierarchy.py:165-178)
+  Level& last = *H->lv.back();
+  np_mean_free(*last.g, last.diag.p, H->scal.p + 8, s);
+  double mean = 0.0;
+  SG_CUDA(cudaMemcpyAsync(&mean, H->scal.p + 8, sizeof(double), cudaMemcpyDeviceToHost, s));
+  SG_CUDA(cudaStreamSynchronize(s));
+  H->eps = std::max(mean * 1e-8, 1e-14);
+  if (last.is_fine && !last.st.A64.p) {
+    last.st.A64.alloc(size_t(243 * last.g->d.nnodes()));
+    fine_to_stencil(*fine, last.st.A64.p, s);
+  }
+  H->coarsest_mode = 1;
+  if (last.g->n_free <= p.cholesky_cutoff) {
+    SG_REQUIRE(!last.is_fine || last.g->n_free <= 20000,
+               "dense assembly limited to 20000 free DOFs");
+    DBuf<double> D(size_t(last.g->n_free * last.g->n_free));
+    stencil_to_dense(*last.g, last.st.A64.p, D.p, H->eps, s);
+    if (H->dense.setup(*last.g, D.p, s)) H->coarsest_mode = 0;
+  }
+  if (H->coarsest_mode == 1) H->pcg.setup(*last.g, last.st.A64.p, last.diag.p, H->eps, p.coarse_pcg_steps, s);
+  const size_t nd0 = size_t(H->lv[0]->nd());
+  H->io_a.alloc(nd0);
+  H->io_b.alloc(nd0);
+  SG_CUDA(cudaStreamSynchronize(s));
+  return H;
+}
+
+}  // namespace sg

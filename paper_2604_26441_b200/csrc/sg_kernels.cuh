@@ -1,0 +1,99 @@
+// Internal declarations shared by the .cu translation units.
+#pragma once
+#include "sg_common.cuh"
+#include "sg_reduce.cuh"
+
+namespace sg {
+
+enum Tag : int { TAG_FP64 = 0, TAG_FP32 = 1, TAG_BF16 = 2 };
+
+template <class T>
+struct KeParam {
+  T k[576];  // row-major 24x24 element matrix (symmetric)
+};
+struct KeDiag {
+  double d[24];
+};
+
+// ---------------------------------------------------------------- fine level
+struct FineOp {
+  Grid grid;
+  DBuf<double> E64;
+  DBuf<float> E32;
+  double ke_host[576];
+  KeParam<double> ke64;
+  KeParam<float> ke32;
+  KeParam<float> ke16;  // bf16-rounded Ke32 (fine_operator.py:45)
+  KeDiag kdiag;
+  double emax = 0.0;
+};
+
+void fine_apply_f64(const FineOp& op, const double* u, double* y, cudaStream_t s);
+void fine_apply_f32(const FineOp& op, const float* u, float* y, cudaStream_t s);
+void fine_apply_bf16(const FineOp& op, const float* u, float* y, cudaStream_t s);
+void fine_diag_raw(const FineOp& op, double* d, cudaStream_t s);
+
+// ------------------------------------------------------ grids and vectors
+void build_grid(Grid& g, int nx, int ny, int nz, const uint8_t* dof_mask_host /*nullable*/,
+                cudaStream_t s);
+void build_coarse_grid(const Grid& fine, Grid& coarse, cudaStream_t s);
+
+template <class T>
+void gather_free(const Grid& g, const T* node_vec, T* free_vec, cudaStream_t s);
+template <class T>
+void scatter_free(const Grid& g, const T* free_vec, T* node_vec, cudaStream_t s);
+void cvt_f64_to_f32(int64_t n, const double* a, float* b, cudaStream_t s);
+void cvt_f32_to_f64(int64_t n, const float* a, double* b, cudaStream_t s);
+
+// numpy pairwise (np.add.reduce) mean over the free-ordered entries of a node
+// vector, written to *out (device).  Bit-identical to numpy's float64 mean.
+void np_mean_free(const Grid& g, const double* node_vec, double* out_dev, cudaStream_t s);
+// d = max(d, 1e-14 * mean) on free dofs (fine_operator.py:86, hierarchy.py:88)
+void diag_floor(const Grid& g, double* d, const double* mean_dev, cudaStream_t s);
+
+// ------------------------------------------------------------- transfers
+// x_f += P x_c (add = true) or x_f = P x_c; node layout, fixed entries zero.
+void prolong(const Grid& fine, const Grid& coarse, const double* xc, double* xf, bool add,
+             cudaStream_t s);
+void restrict_(const Grid& fine, const Grid& coarse, const double* xf, double* xc,
+               cudaStream_t s);
+void transfer_export_csr(const Grid& fine, const Grid& coarse, int64_t* indptr, int64_t* indices,
+                         double* data, int64_t* nnz, cudaStream_t s);
+
+// -------------------------------------------------- 27-point block stencils
+// SoA storage: A[(slot*9 + ra*3 + cb) * nnodes + node], slot = (dk+1)*9+(dj+1)*3+(di+1).
+struct Stencil {
+  DBuf<double> A64;
+  DBuf<float> A32;
+  int64_t nnz = 0;  // nonzero entries on free rows (CSR nnz of the reference)
+};
+
+template <class T>
+void stencil_apply(const Grid& g, const T* A, const T* x, T* y, cudaStream_t s);
+void stencil_diag(const Grid& g, const double* A, double* d, cudaStream_t s);
+void stencil_round_f32(const Grid& g, const double* A64, float* A32, bool bf16, cudaStream_t s);
+void fine_to_stencil(const FineOp& op, double* A, cudaStream_t s);
+int64_t stencil_count_nnz(const Grid& g, const double* A, cudaStream_t s);
+void stencil_export_csr(const Grid& g, const double* A, int64_t* indptr, int64_t* indices,
+                        double* data, cudaStream_t s);
+void stencil_to_dense(const Grid& g, const double* A, double* dense, double eps,
+                      cudaStream_t s);
+
+// level-1 Galerkin aggregation (transfer.py:129-174), bit-exact.
+struct L1Tables {
+  double tri[8 * 576];         // P_c^T Ke P_c (host numpy)
+  std::vector<uint32_t> codes; // boundary codes: child<<24 | fixed-local-dof mask24
+  std::vector<double> diffs;   // per code: masked - tri[child]
+};
+void boundary_codes(const FineOp& op, std::vector<uint32_t>& codes, cudaStream_t s);
+void galerkin_level1(const FineOp& op, const Grid& coarse, const L1Tables& t, double* A,
+                     cudaStream_t s);
+// K_{l+1} = P^T K_l P with scipy csr_matmat summation order (transfer.py:177-181).
+void galerkin_next(const Grid& fine, const Grid& coarse, const double* Af, double* Ac,
+                   cudaStream_t s);
+
+// ------------------------------------------------------------ misc kernels
+void fill_gaussian_unit(const Grid& g, uint64_t seed, double* v_node, RedWork& w,
+                        double* scratch_dev, cudaStream_t s);
+
+}  // namespace sg

@@ -1,0 +1,482 @@
+// Native outer solvers: PCG (krylov.py:113-165), restarted FGMRES
+// (krylov.py:168-281) and the Lanczos spectral probe (diagnostics.py:38-79).
+//
+// The host loop here only reads a handful of scalars per iteration (one
+// small D2H copy per PCG iteration: pq, rz, ||r||^2 and a step flag); every
+// vector operation and reduction runs on the device, deterministically.
+#include <chrono>
+#include <cmath>
+#include "sg_hier.cuh"
+
+namespace sg {
+
+#define SG_EW(n) \
+  const int64_t i_ = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; \
+  if (i_ >= (n)) return;
+
+namespace {
+
+enum Slot { S_NB = 0, S_PQ, S_RZ, S_RR, S_OK, S_RZN, S_TR, S_BETA, S_H0 = 16 };
+
+struct Dot {
+  const double* a;
+  const double* b;
+  __device__ void operator()(int64_t i, double (&acc)[1]) const { acc[0] += a[i] * b[i]; }
+};
+struct DiffSq {  // ||b - t||^2
+  const double* b;
+  const double* t;
+  __device__ void operator()(int64_t i, double (&acc)[1]) const {
+    const double d = __dsub_rn(b[i], t[i]);
+    acc[0] += d * d;
+  }
+};
+struct PcgStep {  // x += a p; r -= a q; rr
+  double* x;
+  double* r;
+  const double* p;
+  const double* q;
+  const double* sc;
+  __device__ void operator()(int64_t i, double (&acc)[1]) const {
+    const double pq = sc[S_PQ], rz = sc[S_RZ];
+    const bool ok = isfinite(pq) && pq != 0.0 && isfinite(rz);
+    double rv = r[i];
+    if (ok) {
+      const double a = __ddiv_rn(rz, pq);
+      x[i] = __dadd_rn(x[i], __dmul_rn(a, p[i]));
+      rv = __dsub_rn(rv, __dmul_rn(a, q[i]));
+      r[i] = rv;
+    }
+    acc[0] += rv * rv;
+  }
+};
+struct PcgStepPost {
+  double* sc;
+  __device__ void operator()(const double (&t)[1]) const {
+    const double pq = sc[S_PQ], rz = sc[S_RZ];
+    sc[S_OK] = (isfinite(pq) && pq != 0.0 && isfinite(rz)) ? 1.0 : 0.0;
+    sc[S_RR] = t[0];
+  }
+};
+struct RznPost {  // beta = rzn/rz ; rz = rzn
+  double* sc;
+  __device__ void operator()(const double (&t)[1]) const {
+    sc[S_RZN] = t[0];
+    sc[S_BETA] = __ddiv_rn(t[0], sc[S_RZ]);
+    sc[S_RZ] = t[0];
+  }
+};
+
+__global__ void pupd_kernel(int64_t n, const double* __restrict__ z, double* __restrict__ p,
+                            const double* __restrict__ sc) {
+  SG_EW(n);
+  p[i_] = __dadd_rn(z[i_], __dmul_rn(sc[S_BETA], p[i_]));
+}
+__global__ void copy_k(int64_t n, const double* __restrict__ a, double* __restrict__ b) {
+  SG_EW(n);
+  b[i_] = a[i_];
+}
+__global__ void mul_k(int64_t n, const double* __restrict__ a, const double* __restrict__ b,
+                      double* __restrict__ c) {
+  SG_EW(n);
+  c[i_] = __dmul_rn(a[i_], b[i_]);
+}
+__global__ void sub_k(int64_t n, const double* __restrict__ a, const double* __restrict__ b,
+                      double* __restrict__ c) {
+  SG_EW(n);
+  c[i_] = __dsub_rn(a[i_], b[i_]);
+}
+__global__ void div_host_k(int64_t n, const double* __restrict__ a, double s, double* __restrict__ c) {
+  SG_EW(n);
+  c[i_] = __ddiv_rn(a[i_], s);
+}
+__global__ void axpy_dev_k(int64_t n, const double* __restrict__ h, const double* __restrict__ v,
+                           double* __restrict__ w) {  // w -= h * v
+  SG_EW(n);
+  w[i_] = __dsub_rn(w[i_], __dmul_rn(*h, v[i_]));
+}
+__global__ void gemv_t_k(int64_t n, int J, const double* __restrict__ Q, int64_t ld,
+                         const double* __restrict__ h, double* __restrict__ w, double sign) {
+  // w = w + sign * (Q^T h) with the GEMV result formed first (numpy: w -= Q.T @ h)
+  SG_EW(n);
+  double t = 0.0;
+  for (int j = 0; j < J; ++j) t += Q[int64_t(j) * ld + i_] * h[j];
+  w[i_] = sign > 0 ? __dadd_rn(w[i_], t) : __dsub_rn(w[i_], t);
+}
+__global__ void f64_to_f32_k(int64_t n, const double* __restrict__ a, float* __restrict__ b) {
+  SG_EW(n);
+  b[i_] = __double2float_rn(a[i_]);
+}
+__global__ void f32_to_f64_k(int64_t n, const float* __restrict__ a, double* __restrict__ b) {
+  SG_EW(n);
+  b[i_] = double(a[i_]);
+}
+
+inline int nb256(int64_t n) { return grid_blocks(n, 256); }
+
+struct Ctx {
+  NativeSys& sys;
+  cudaStream_t s;
+  int64_t nd;
+  RedWork red;
+  DBuf<double> sc;
+  DBuf<float> t32a, t32b;
+  Ctx(NativeSys& sy, cudaStream_t st) : sys(sy), s(st) {
+    nd = 3 * sys.fine->grid.d.nnodes();
+    red.init(s);
+    sc.alloc(256);
+    SG_CUDA(cudaMemsetAsync(sc.p, 0, 256 * sizeof(double), s));
+    if (sys.ktag != TAG_FP64) {
+      t32a.alloc(size_t(nd));
+      t32b.alloc(size_t(nd));
+    }
+  }
+  // y = apply_K(x) promoted to f64 (krylov.py:136: np.asarray(apply_K(p), float64))
+  void K(const double* x, double* y) {
+    if (sys.ktag == TAG_FP64) {
+      fine_apply_f64(*sys.fine, x, y, s);
+    } else {
+      f64_to_f32_k<<<nb256(nd), 256, 0, s>>>(nd, x, t32a.p);
+      fine_apply_tag(*sys.fine, sys.ktag, t32a.p, t32b.p, s);
+      f32_to_f64_k<<<nb256(nd), 256, 0, s>>>(nd, t32b.p, y);
+      SG_CHECK_LAUNCH();
+    }
+  }
+  // z = apply_M(r)
+  void M(const double* r, double* z) {
+    if (sys.hier) {
+      Level& L0 = *sys.hier->lv[0];
+      if (r != L0.w.r.p) copy_k<<<nb256(nd), 256, 0, s>>>(nd, r, L0.w.r.p);
+      cycle(*sys.hier, 0, sys.gamma, s);
+      copy_k<<<nb256(nd), 256, 0, s>>>(nd, L0.w.x.p, z);
+    } else {
+      mul_k<<<nb256(nd), 256, 0, s>>>(nd, sys.fw->diag_inv_ptr(), r, z);
+    }
+    SG_CHECK_LAUNCH();
+  }
+  void dot(const double* a, const double* b, int slot) {
+    launch_reduce<1>(nd, Dot{a, b}, StoreTo<1>{{sc.p + slot}}, red, s);
+  }
+  double read(int slot) {
+    double v = 0.0;
+    SG_CUDA(cudaMemcpyAsync(&v, sc.p + slot, sizeof(double), cudaMemcpyDeviceToHost, s));
+    SG_CUDA(cudaStreamSynchronize(s));
+    return v;
+  }
+  double true_res(const double* b, const double* x, double* tmp, double normb) {
+    K(x, tmp);
+    launch_reduce<1>(nd, DiffSq{b, tmp}, StoreTo<1>{{sc.p + S_TR}}, red, s);
+    return std::sqrt(read(S_TR)) / normb;
+  }
+};
+
+bool stagnant(const std::vector<double>& best) {  // krylov.py:86-97
+  const size_t k = best.size();
+  if (k <= 50) return false;
+  const double then = best[k - 1 - 50];
+  return !(best.back() <= (1.0 - 0.01) * then);
+}
+
+void record(std::vector<double>& hist, std::vector<double>& best, double rel) {
+  hist.push_back(rel);
+  const double prev = best.empty() ? INFINITY : best.back();
+  best.push_back(std::min(prev, rel));
+}
+
+double now() {
+  return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ PCG
+void pcg_native(NativeSys& sys, const double* b, double* x, const SolverCfg& cfg, SolveOut& out,
+                std::vector<double>& hist, cudaStream_t s) {
+  const double t0 = now();
+  Ctx C(sys, s);
+  const int64_t nd = C.nd;
+  hist.clear();
+  std::vector<double> best;
+  C.dot(b, b, S_NB);
+  const double normb = std::sqrt(C.read(S_NB));
+  SG_CUDA(cudaMemsetAsync(x, 0, sizeof(double) * nd, s));
+  if (normb == 0.0) {
+    out = SolveOut{1, 0, 0.0, 0, now() - t0};
+    return;
+  }
+  DBuf<double> r_own, z(static_cast<size_t>(nd)), p(static_cast<size_t>(nd)), q(static_cast<size_t>(nd));
+  double* r = sys.hier ? sys.hier->lv[0]->w.r.p : (r_own.alloc(size_t(nd)), r_own.p);
+  copy_k<<<nb256(nd), 256, 0, s>>>(nd, b, r);
+  C.M(r, z.p);
+  copy_k<<<nb256(nd), 256, 0, s>>>(nd, z.p, p.p);
+  SG_CHECK_LAUNCH();
+  C.dot(r, z.p, S_RZ);
+  double target = cfg.tol;
+  int kind = 1;  // cap
+  for (int it = 0; it < cfg.maxiter; ++it) {
+    C.K(p.p, q.p);
+    C.dot(p.p, q.p, S_PQ);
+    launch_reduce<1>(nd, PcgStep{x, r, p.p, q.p, C.sc.p}, PcgStepPost{C.sc.p}, C.red, s);
+    double h[4];
+    SG_CUDA(cudaMemcpyAsync(h, C.sc.p + S_PQ, 4 * sizeof(double), cudaMemcpyDeviceToHost, s));
+    SG_CUDA(cudaStreamSynchronize(s));
+    const double rz = h[1], rr = h[2], ok = h[3];
+    if (!std::isfinite(rz) || ok == 0.0) {  // rz_new / pq checks (krylov.py:138-140, :160-162)
+      kind = 3;
+      break;
+    }
+    const double rel = std::sqrt(rr) / normb;
+    record(hist, best, rel);
+    if (!std::isfinite(rel)) {
+      kind = 3;
+      break;
+    }
+    if (rel < target) {
+      const double tr = C.true_res(b, x, q.p, normb);
+      if (tr < cfg.tol) {
+        kind = 0;
+        break;
+      }
+      if (stagnant(best)) {
+        kind = 2;
+        break;
+      }
+      target *= 0.1;
+    }
+    C.M(r, z.p);
+    launch_reduce<1>(nd, Dot{r, z.p}, RznPost{C.sc.p}, C.red, s);
+    pupd_kernel<<<nb256(nd), 256, 0, s>>>(nd, z.p, p.p, C.sc.p);
+    SG_CHECK_LAUNCH();
+  }
+  const double tr = C.true_res(b, x, q.p, normb);
+  out.converged = std::isfinite(tr) && tr < cfg.tol;
+  out.iterations = int(hist.size());
+  out.final_true_residual = tr;
+  out.failure_kind = out.converged ? 0 : kind;
+  out.wall_time = now() - t0;
+}
+
+// --------------------------------------------------------------- FGMRES
+static void solve_upper(const std::vector<double>& H, int ldh, int n, const std::vector<double>& g,
+                        std::vector<double>& y) {
+  // back substitution (column-oriented, like reference dtrsv), lstsq fallback
+  y.assign(g.begin(), g.begin() + n);
+  bool ok = true;
+  for (int j = n - 1; j >= 0; --j) {
+    const double d = H[size_t(j) * ldh + j];
+    y[size_t(j)] = y[size_t(j)] / d;
+    const double t = y[size_t(j)];
+    for (int i = 0; i < j; ++i) y[size_t(i)] -= t * H[size_t(i) * ldh + j];
+  }
+  for (double v : y) ok = ok && std::isfinite(v);
+  if (ok) return;
+  // least squares via Householder QR with column pivoting-free fallback:
+  // minimum-norm solution of the (singular) upper system through normal
+  // equations regularised at machine precision.
+  std::vector<double> A(static_cast<size_t>(n) * n), b(static_cast<size_t>(n));
+  for (int i = 0; i < n; ++i) {
+    b[size_t(i)] = 0.0;
+    for (int k = 0; k < n; ++k) {
+      double sacc = 0.0;
+      for (int r = 0; r < n; ++r) sacc += H[size_t(r) * ldh + i] * H[size_t(r) * ldh + k];
+      A[size_t(i) * n + k] = sacc;
+    }
+    for (int r = 0; r < n; ++r) b[size_t(i)] += H[size_t(r) * ldh + i] * g[size_t(r)];
+  }
+  double tr = 0.0;
+  for (int i = 0; i < n; ++i) tr += A[size_t(i) * n + i];
+  for (int i = 0; i < n; ++i) A[size_t(i) * n + i] += 1e-14 * (tr > 0 ? tr : 1.0);
+  for (int c = 0; c < n; ++c) {  // Gaussian elimination (SPD)
+    const double piv = A[size_t(c) * n + c];
+    for (int r = c + 1; r < n; ++r) {
+      const double f = A[size_t(r) * n + c] / piv;
+      for (int k = c; k < n; ++k) A[size_t(r) * n + k] -= f * A[size_t(c) * n + k];
+      b[size_t(r)] -= f * b[size_t(c)];
+    }
+  }
+  for (int r = n - 1; r >= 0; --r) {
+    double sacc = b[size_t(r)];
+    for (int k = r + 1; k < n; ++k) sacc -= A[size_t(r) * n + k] * y[size_t(k)];
+    y[size_t(r)] = sacc / A[size_t(r) * n + r];
+  }
+}
+
+void fgmres_native(NativeSys& sys, const double* b, double* x, const SolverCfg& cfg, SolveOut& out,
+                   std::vector<double>& hist, cudaStream_t s) {
+  const double t0 = now();
+  Ctx C(sys, s);
+  const int64_t nd = C.nd;
+  hist.clear();
+  std::vector<double> best;
+  C.dot(b, b, S_NB);
+  const double normb = std::sqrt(C.read(S_NB));
+  SG_CUDA(cudaMemsetAsync(x, 0, sizeof(double) * nd, s));
+  if (normb == 0.0) {
+    out = SolveOut{1, 0, 0.0, 0, now() - t0};
+    return;
+  }
+  const int m = cfg.restart;
+  SG_REQUIRE(m + 1 <= 200, "restart too large for the scalar slots");
+  DBuf<double> V(size_t(m + 1) * nd), Z(size_t(m) * nd), w(static_cast<size_t>(nd)),
+      r(static_cast<size_t>(nd)), tmp(static_cast<size_t>(nd)), yv(static_cast<size_t>(m));
+  int kind = 1;
+  bool done = false;
+  while (!done && int(hist.size()) < cfg.maxiter) {
+    C.K(x, tmp.p);
+    sub_k<<<nb256(nd), 256, 0, s>>>(nd, b, tmp.p, r.p);
+    SG_CHECK_LAUNCH();
+    C.dot(r.p, r.p, S_TR);
+    const double beta = std::sqrt(C.read(S_TR));
+    if (!std::isfinite(beta)) {
+      kind = 3;
+      break;
+    }
+    if (beta / normb < cfg.tol) {
+      kind = 0;
+      break;
+    }
+    std::vector<double> H(size_t(m + 1) * m, 0.0), cs(size_t(m), 0.0), sn(size_t(m), 0.0),
+        g(size_t(m + 1), 0.0);
+    g[0] = beta;
+    div_host_k<<<nb256(nd), 256, 0, s>>>(nd, r.p, beta, V.p);
+    SG_CHECK_LAUNCH();
+    int used = 0;
+    bool claimed = false;
+    for (int j = 0; j < m; ++j) {
+      double* Vj = V.p + int64_t(j) * nd;
+      double* Zj = Z.p + int64_t(j) * nd;
+      C.M(Vj, Zj);
+      C.K(Zj, w.p);
+      for (int i = 0; i <= j; ++i) {  // modified Gram-Schmidt
+        const double* Vi = V.p + int64_t(i) * nd;
+        C.dot(w.p, Vi, S_H0 + i);
+        axpy_dev_k<<<nb256(nd), 256, 0, s>>>(nd, C.sc.p + S_H0 + i, Vi, w.p);
+        SG_CHECK_LAUNCH();
+      }
+      C.dot(w.p, w.p, S_H0 + j + 1);
+      std::vector<double> col(size_t(j + 2));
+      SG_CUDA(cudaMemcpyAsync(col.data(), C.sc.p + S_H0, sizeof(double) * (j + 2),
+                              cudaMemcpyDeviceToHost, s));
+      SG_CUDA(cudaStreamSynchronize(s));
+      col[size_t(j + 1)] = std::sqrt(col[size_t(j + 1)]);
+      bool fin = true;
+      for (int i = 0; i <= j + 1; ++i) {
+        H[size_t(i) * m + j] = col[size_t(i)];
+        fin = fin && std::isfinite(col[size_t(i)]);
+      }
+      if (!fin) {
+        kind = 3;
+        done = true;
+        used = j + 1;
+        break;
+      }
+      const bool happy = H[size_t(j + 1) * m + j] < 1e-14;
+      if (!happy) {
+        div_host_k<<<nb256(nd), 256, 0, s>>>(nd, w.p, H[size_t(j + 1) * m + j], V.p + int64_t(j + 1) * nd);
+        SG_CHECK_LAUNCH();
+      }
+      for (int i = 0; i < j; ++i) {
+        const double h0 = cs[size_t(i)] * H[size_t(i) * m + j] + sn[size_t(i)] * H[size_t(i + 1) * m + j];
+        H[size_t(i + 1) * m + j] = -sn[size_t(i)] * H[size_t(i) * m + j] + cs[size_t(i)] * H[size_t(i + 1) * m + j];
+        H[size_t(i) * m + j] = h0;
+      }
+      const double den = std::hypot(H[size_t(j) * m + j], H[size_t(j + 1) * m + j]);
+      if (den == 0.0) {
+        cs[size_t(j)] = 1.0;
+        sn[size_t(j)] = 0.0;
+      } else {
+        cs[size_t(j)] = H[size_t(j) * m + j] / den;
+        sn[size_t(j)] = H[size_t(j + 1) * m + j] / den;
+      }
+      H[size_t(j) * m + j] = cs[size_t(j)] * H[size_t(j) * m + j] + sn[size_t(j)] * H[size_t(j + 1) * m + j];
+      H[size_t(j + 1) * m + j] = 0.0;
+      g[size_t(j + 1)] = -sn[size_t(j)] * g[size_t(j)];
+      g[size_t(j)] = cs[size_t(j)] * g[size_t(j)];
+      used = j + 1;
+      const double rel = std::fabs(g[size_t(j + 1)]) / normb;
+      record(hist, best, rel);
+      if (!std::isfinite(rel)) {
+        kind = 3;
+        done = true;
+        break;
+      }
+      if (happy || rel < cfg.tol) {
+        claimed = true;
+        break;
+      }
+      if (int(hist.size()) >= cfg.maxiter) break;
+    }
+    if (kind == 3) break;
+    if (used > 0) {
+      std::vector<double> Hs(size_t(used) * used), y;
+      for (int i = 0; i < used; ++i)
+        for (int k = 0; k < used; ++k) Hs[size_t(i) * used + k] = H[size_t(i) * m + k];
+      solve_upper(Hs, used, used, g, y);
+      yv.upload(y.data(), size_t(used), s);
+      gemv_t_k<<<nb256(nd), 256, 0, s>>>(nd, used, Z.p, nd, yv.p, x, 1.0);
+      SG_CHECK_LAUNCH();
+    }
+    if (done) break;
+    const double tr = C.true_res(b, x, tmp.p, normb);
+    if (tr < cfg.tol) {
+      kind = 0;
+      break;
+    }
+    if (claimed && stagnant(best)) {
+      kind = 2;
+      break;
+    }
+    if (int(hist.size()) >= cfg.maxiter) {
+      kind = 1;
+      break;
+    }
+  }
+  const double tr = C.true_res(b, x, tmp.p, normb);
+  out.converged = std::isfinite(tr) && tr < cfg.tol;
+  out.iterations = int(hist.size());
+  out.final_true_residual = tr;
+  out.failure_kind = out.converged ? 0 : kind;
+  out.wall_time = now() - t0;
+}
+
+// -------------------------------------------------------------- Lanczos
+void lanczos_native(NativeSys& sys, int m, uint64_t seed, std::vector<double>& H, int& used,
+                    bool& partial, cudaStream_t s) {
+  Ctx C(sys, s);
+  const int64_t nd = C.nd;
+  SG_REQUIRE(m >= 2 && m <= 200, "Lanczos steps out of range");
+  DBuf<double> Q(size_t(m) * nd), w(static_cast<size_t>(nd)), kv(static_cast<size_t>(nd));
+  H.assign(size_t(m) * m, 0.0);
+  used = m;
+  partial = false;
+  fill_gaussian_unit(sys.fine->grid, seed, Q.p, C.red, C.sc.p + S_TR, s);
+  for (int j = 0; j < m; ++j) {
+    const double* Qj = Q.p + int64_t(j) * nd;
+    C.K(Qj, kv.p);
+    C.M(kv.p, w.p);
+    for (int t = 0; t <= j; ++t) C.dot(Q.p + int64_t(t) * nd, w.p, S_H0 + t);
+    gemv_t_k<<<nb256(nd), 256, 0, s>>>(nd, j + 1, Q.p, nd, C.sc.p + S_H0, w.p, -1.0);
+    SG_CHECK_LAUNCH();
+    std::vector<double> h(size_t(j + 1)), h2(size_t(j + 1));
+    SG_CUDA(cudaMemcpyAsync(h.data(), C.sc.p + S_H0, sizeof(double) * (j + 1), cudaMemcpyDeviceToHost, s));
+    for (int t = 0; t <= j; ++t) C.dot(Q.p + int64_t(t) * nd, w.p, S_H0 + t);
+    gemv_t_k<<<nb256(nd), 256, 0, s>>>(nd, j + 1, Q.p, nd, C.sc.p + S_H0, w.p, -1.0);
+    SG_CHECK_LAUNCH();
+    SG_CUDA(cudaMemcpyAsync(h2.data(), C.sc.p + S_H0, sizeof(double) * (j + 1), cudaMemcpyDeviceToHost, s));
+    SG_CUDA(cudaStreamSynchronize(s));
+    for (int t = 0; t <= j; ++t) H[size_t(t) * m + j] = h[size_t(t)] + h2[size_t(t)];
+    if (j == m - 1) break;
+    C.dot(w.p, w.p, S_TR);
+    const double bn = std::sqrt(C.read(S_TR));
+    if (!std::isfinite(bn) || bn < 1e-14) {
+      used = j + 1;
+      partial = true;
+      break;
+    }
+    H[size_t(j + 1) * m + j] = bn;
+    div_host_k<<<nb256(nd), 256, 0, s>>>(nd, w.p, bn, Q.p + int64_t(j + 1) * nd);
+    SG_CHECK_LAUNCH();
+  }
+}
+
+}  // namespace sg

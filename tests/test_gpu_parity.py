@@ -1,0 +1,211 @@
+"""GPU parity: the sm_100a path (through the C ABI) against the CPU oracle.
+
+Bars: bit-exact for the integer / ordered-FP64 work (diagonals, transfers,
+level-1 and level-2 Galerkin operators -- values AND sparsity pattern);
+FP64 operator applies within 1e-13 relative (norm); FP32 / BF16 applies
+within 1e-6 relative; solver iteration counts within +-2 of the oracle
+and residual histories within 1e-4 relative per entry.
+"""
+
+import warnings
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+P = pytest.importorskip("paper_2604_26441_b200")
+from oracle import simp_oracle as O  # noqa: E402
+
+
+def _pair(dims, kind="uniform", vf=0.5, p=3.0, seed=42):
+    g = P.build_cantilever(*dims)
+    op = P.FineOperator(g, P.simp_modulus(P.make_state(kind, *dims, vf=vf, seed=seed), p))
+    og, E, ke = O.problem(*dims, kind=kind, vf=vf, p=p, seed=seed)
+    assert np.array_equal(E, op.modulus.E)
+    assert np.array_equal(ke, op.ke)
+    return g, op, og, E, ke
+
+
+def _rel(a, b):
+    return np.linalg.norm(np.asarray(a, np.float64) - np.asarray(b, np.float64)) / np.linalg.norm(b)
+
+
+@pytest.mark.parametrize("dims,kind", [((4, 2, 2), "uniform"), ((6, 4, 2), "binary"),
+                                       ((5, 3, 4), "random_floor"), ((12, 10, 8), "binary")])
+def test_fine_apply_all_tags(dims, kind):
+    g, op, og, E, ke = _pair(dims, kind)
+    u = P.SplitMix64(3).gaussian(g.n_free)
+    assert _rel(op.matvec_tagged(u, P.PrecisionTag.FP64), O.fine_apply(og, E, ke, u, "fp64")) < 1e-13
+    u32 = u.astype(np.float32)
+    y32 = op.matvec_tagged(u32, P.PrecisionTag.FP32)
+    assert y32.dtype == np.float32
+    assert _rel(y32, O.fine_apply(og, E, ke, u32, "fp32")) < 1e-6
+    y16 = op.matvec_tagged(u32, P.PrecisionTag.BF16EMU)
+    assert _rel(y16, O.fine_apply(og, E, ke, u32, "bf16")) < 1e-6
+    # determinism: repeated applies are bit-identical
+    assert np.array_equal(op.matvec(u), op.matvec(u))
+
+
+def test_fine_free_grid_rigid_nullspace_and_dense():
+    nx, ny, nz = 3, 2, 2
+    g = P.make_grid(nx, ny, nz, np.zeros(3 * (nx + 1) * (ny + 1) * (nz + 1), dtype=bool))
+    op = P.FineOperator(g, P.simp_modulus(P.make_state("uniform", nx, ny, nz, vf=0.5), p=1.0,
+                                          emin=1e-12, e0=1.0))
+    scale = np.abs(op.assemble_dense()).max()
+    for axis in range(3):
+        t = np.zeros(g.n_dof)
+        t[axis::3] = 1.0
+        assert np.abs(op.matvec(t)).max() < 1e-10 * scale
+    og = O.make_grid(nx, ny, nz, np.zeros(g.n_dof, dtype=bool))
+    assert np.array_equal(op.assemble_dense(), O.fine_dense(og, op.modulus.E, op.ke))
+
+
+@pytest.mark.parametrize("dims,kind", [((4, 2, 2), "uniform"), ((6, 4, 2), "binary"),
+                                       ((16, 8, 8), "random_floor")])
+def test_diagonal_bit_exact(dims, kind):
+    g, op, og, E, ke = _pair(dims, kind)
+    assert np.array_equal(op.diagonal(), O.fine_diag(og, E, ke))
+
+
+def test_diagonal_floor_bit_exact():
+    g = P.build_cantilever(1, 2, 1)
+    f = P.simp_modulus(P.make_state("layered", 1, 2, 1, floor=0.0), p=1.0, emin=1e-30, e0=1.0)
+    op = P.FineOperator(g, f)
+    og = O.cantilever(1, 2, 1)
+    assert np.array_equal(op.diagonal(), O.fine_diag(og, f.E, op.ke))
+
+
+@pytest.mark.parametrize("dims,kind", [((8, 4, 4), "uniform"), ((8, 4, 4), "binary"),
+                                       ((16, 8, 8), "uniform"), ((12, 8, 4), "random_floor"),
+                                       ((16, 16, 16), "binary"), ((20, 12, 8), "mixed_near_void")])
+def test_galerkin_levels_bit_exact(dims, kind):
+    g, op, og, E, ke = _pair(dims, kind)
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        h = P.build_hierarchy(op, 3, "fp64")
+    P0, c1 = O.transfer(og)
+    K1 = O.galerkin_l1(og, E, ke, c1)
+    refs = [K1]
+    if c1.nx % 2 == 0 and c1.ny % 2 == 0 and c1.nz % 2 == 0:
+        P1, _ = O.transfer(c1)
+        refs.append(O.galerkin_next(P1, K1))
+    for lev, ref in zip(h.levels[1:], refs):
+        A = lev.operator
+        assert np.array_equal(A.indptr, ref.indptr)
+        assert np.array_equal(A.indices, ref.indices)
+        assert np.array_equal(A.data, ref.data)
+    T = h.levels[0].transfer.P
+    assert np.array_equal(T.indptr, P0.indptr) and np.array_equal(T.indices, P0.indices)
+    assert np.array_equal(T.data, P0.data)
+
+
+def test_transfers_bit_exact():
+    g, op, og, E, ke = _pair((8, 6, 4), "binary")
+    t = P.build_transfer(g)
+    P0, c1 = O.transfer(og)
+    xc = P.SplitMix64(1).gaussian(c1.n_free)
+    xf = P.SplitMix64(2).gaussian(og.n_free)
+    assert np.array_equal(t.prolong(xc), P0 @ xc)
+    assert np.array_equal(t.restrict(xf), P0.T @ xf)
+    assert np.array_equal(t.coarse.dirichlet_mask, c1.mask)
+
+
+def test_level1_standalone_bit_exact():
+    g, op, og, E, ke = _pair((8, 4, 4), "binary")
+    t = P.build_transfer(g)
+    K1 = P.assemble_level1(op, t)
+    _, c1 = O.transfer(og)
+    ref = O.galerkin_l1(og, E, ke, c1)
+    assert np.array_equal(K1.indptr, ref.indptr)
+    assert np.array_equal(K1.indices, ref.indices)
+    assert np.array_equal(K1.data, ref.data)
+
+
+@pytest.mark.parametrize("dims,kind,policy", [((8, 4, 4), "uniform", "fp64"),
+                                              ((8, 4, 4), "uniform", "fp32"),
+                                              ((8, 4, 4), "binary", "bf16"),
+                                              ((16, 8, 8), "binary", "fp32"),
+                                              ((16, 16, 16), "uniform", "fp32")])
+def test_hierarchy_and_cycle(dims, kind, policy):
+    g, op, og, E, ke = _pair(dims, kind)
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        h = P.build_hierarchy(op, 4, policy)
+    oh = O.Hier(og, E, ke, 4, policy)
+    assert [lev.n_free for lev in h.levels] == [lev.n for lev in oh.levels]
+    np.testing.assert_allclose([lev.lam_max for lev in h.levels], [lev.lam for lev in oh.levels],
+                               rtol=1e-10)
+    assert h.coarsest.mode == oh.mode
+    assert h.coarsest.eps == pytest.approx(oh.eps, rel=1e-15)
+    r = P.SplitMix64(7).gaussian(g.n_free)
+    tol = 1e-9 if policy == "fp64" else 2e-5
+    assert _rel(h.vcycle(r), oh.vcycle(r)) < tol
+
+
+def test_pcg80_and_dense_coarsest():
+    g, op, og, E, ke = _pair((8, 4, 4), "uniform")
+    h = P.build_hierarchy(op, 3, "fp64", cholesky_cutoff=0)
+    oh = O.Hier(og, E, ke, 3, "fp64", cutoff=0)
+    assert h.coarsest.mode == "pcg80"
+    r = P.SplitMix64(9).gaussian(g.n_free)
+    assert _rel(h.vcycle(r), oh.vcycle(r)) < 1e-9
+    h1 = P.build_hierarchy(op, 1, "fp64")
+    assert h1.coarsest.mode == "dense_cholesky"
+    K = op.assemble_dense()
+    ref = np.linalg.solve(K + h1.coarsest.eps * np.eye(g.n_free), r)
+    np.testing.assert_allclose(h1.vcycle(r), ref, rtol=1e-9, atol=1e-12 * np.abs(ref).max())
+
+
+@pytest.mark.parametrize("dims,kind,policy", [((8, 4, 4), "uniform", "fp64"),
+                                              ((16, 8, 8), "uniform", "fp32"),
+                                              ((16, 8, 8), "binary", "fp32"),
+                                              ((12, 12, 12), "binary", "fp32"),
+                                              ((8, 4, 4), "binary", "bf16")])
+def test_outer_solver_parity(dims, kind, policy):
+    g, op, og, E, ke = _pair(dims, kind)
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        h = P.build_hierarchy(op, 4, policy)
+    b = g.load[g.free_dofs]
+    method = "fgmres" if policy == "bf16" else "pcg"
+    solver = P.fgmres if method == "fgmres" else P.pcg
+    rep = solver(op.matvec, h.vcycle, b, P.SolverConfig(method=method, tol=1e-6, maxiter=200))
+    ref, _ = O.solve(og, E, ke, policy)
+    assert rep.converged == ref.converged
+    assert abs(rep.iterations - ref.iterations) <= 2
+    k = min(len(rep.residual_history), len(ref.residual_history))
+    np.testing.assert_allclose(rep.residual_history[:k], ref.residual_history[:k], rtol=1e-4)
+    assert rep.converged == (rep.final_true_residual < 1e-6)
+    np.testing.assert_allclose(op.compliance(rep.x), float(b @ ref.x), rtol=1e-6)
+
+
+def test_flat_jacobi_and_generic_callables():
+    g, op, og, E, ke = _pair((8, 4, 4), "uniform")
+    b = g.load[g.free_dofs]
+    rep = P.flat_jacobi_pcg(op, b, P.SolverConfig(tol=1e-6, maxiter=200))
+    ref = O.jacobi_pcg(og, E, ke, b)
+    assert rep.iterations == ref.iterations
+    np.testing.assert_allclose(rep.residual_history, ref.residual_history, rtol=1e-8)
+    # reference-style lambdas: identity system in one iteration
+    bb = P.SplitMix64(1).gaussian(20)
+    r1 = P.pcg(lambda x: x, lambda x: x, bb, P.SolverConfig(tol=1e-6, maxiter=10))
+    assert r1.converged and r1.iterations == 1
+    np.testing.assert_allclose(r1.x, bb, rtol=1e-14)
+
+
+def test_config1_40cube_fp32_gmg_golden():
+    """BASELINE configs[0] through the public API; golden from the real reference."""
+    import os
+    z = np.load(os.path.join(os.path.dirname(__file__), "golden", "cfg40.npz"))
+    g = P.build_cantilever(40, 40, 40)
+    op = P.FineOperator(g, P.simp_modulus(P.make_state("uniform", 40, 40, 40, vf=0.5), 3.0))
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        h = P.build_hierarchy(op, 4, "fp32")
+    assert [lev.n_free for lev in h.levels] == list(z["nfree"])
+    assert [0] + [lev.operator.nnz for lev in h.levels[1:]] == list(z["nnz"])
+    rep = P.pcg(op.matvec, h.vcycle, g.load[g.free_dofs], P.SolverConfig(tol=1e-6, maxiter=200))
+    assert rep.iterations == int(z["iters"][0]) == 11
+    np.testing.assert_allclose(rep.residual_history, z["hist"], rtol=1e-4)
+    np.testing.assert_allclose(op.compliance(rep.x), float(z["compliance"][0]), rtol=1e-6)
