@@ -1,0 +1,328 @@
+"""Benchmark of the PCG / GMG hot path (BASELINE.json metric).
+
+Workload (configs[3]): 100x100x100 (1M elements) cantilever, uniform rho=0.5,
+p=3, FP32-GMG (policy "fp32", 4 levels requested -> 3 after the odd-dim
+clamp, pcg80 coarsest), PCG to tol 1e-6, cap 200.  One step = one full PCG
+solve; the hierarchy is built once outside the timed region ("setup
+excluded", as the metric says).  value = seconds per solve (device time,
+CUDA events on the launch stream, max over ranks); e2e = the same solve
+through the public Python API with the right-hand side in host memory and
+the solution copied back (H2D + D2H inside the timed region).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference] [--size 100]
+
+--impl reference times the CPU oracle port (oracle/simp_oracle.py, a numpy/
+scipy restatement of the reference package, which is pure Python and so has
+no compiled artefact) on the host cores: one step = one PCG iteration of the
+same 100^3 problem (V-cycle + FP64 fine apply + vector updates), scaled by
+the oracle's own iteration count to seconds per solve.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+import warnings
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+HBM_FALLBACK = 6650.0
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            d = json.load(fh)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return HBM_FALLBACK, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clock / throttle sampling during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), "--query-gpu=" + self.FIELDS,
+                                      "--format=csv,noheader,nounits"], capture_output=True,
+                                     text=True, timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([v.strip() for v in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        import statistics
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4)
+                          if len(r) > 3 + i and r[3 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+def _dist():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def oracle_iterations(N, steps, warmup, full_solve=False):
+    """Time `steps` PCG iterations (krylov.py:135-164 loop body: FP64 fine apply,
+    dots, axpys, V-cycle) of the CPU oracle at N^3 after `warmup` untimed ones."""
+    import numpy as np
+    from oracle import simp_oracle as O
+    t0 = time.perf_counter()
+    g, E, ke = O.problem(N, N, N)
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        h = O.Hier(g, E, ke, 4, "fp32")
+    setup = time.perf_counter() - t0
+    b = g.load[g.free]
+    Kf = lambda v: O.fine_apply(g, E, ke, v, "fp64")
+    full = O.pcg(Kf, h.vcycle, b, 1e-6, 200) if full_solve else None
+    x = np.zeros_like(b)
+    r = b.copy()
+    p = h.vcycle(r)
+    rz = float(r @ p)
+    samples = []
+    for k in range(warmup + steps):
+        s = time.perf_counter()
+        q = Kf(p)
+        a = rz / float(p @ q)
+        x = x + a * p
+        r = r - a * q
+        float(np.linalg.norm(r) / np.linalg.norm(b))
+        z = h.vcycle(r)
+        rzn = float(r @ z)
+        p = z + (rzn / rz) * p
+        rz = rzn
+        if k >= warmup:
+            samples.append(time.perf_counter() - s)
+    return {"per_iter_s": sum(samples) / len(samples), "setup_s": setup,
+            "iters_timed": len(samples), "full": full}
+
+
+def run_reference(args):
+    world, rank, _ = _dist()
+    if rank != 0:
+        return 0
+    N = args.size
+    res = oracle_iterations(N, args.steps, args.warmup, full_solve=True)
+    full = res["full"]
+    n_iters = full.iterations
+    per_iter = res["per_iter_s"]
+    setup = res["setup_s"]
+    value = per_iter * n_iters
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": per_iter * 1e3, "higher_is_better": False, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64/f32 (FP32-GMG)", "data": "synthetic",
+        "config": _config(args),
+        "cpu_baseline": {"value": value, "unit": "s", "cores": os.cpu_count(), "kind": "port",
+                         "sample": f"{res['iters_timed']} PCG iterations (V-cycle + FP64 apply) of the "
+                                   f"{N}^3 oracle, scaled by its {n_iters}-iteration full solve"},
+        "e2e": {"value": value, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "oracle_setup_s": setup,
+        "oracle_full_solve_s": full.wall_time,
+        "oracle_iterations": n_iters,
+        "oracle_converged": bool(full.converged),
+    }
+    print(json.dumps(line))
+    return 0
+
+
+METRIC = "GMG-PCG solve s at 1M elements; fine matvec achieved HBM GB/s; PCG iters"
+
+
+def _config(args):
+    N = args.size
+    return {"workload": f"{N}x{N}x{N} uniform rho=0.5 p=3 cantilever, FP32-GMG PCG (tol 1e-6, cap 200)",
+            "elements": N ** 3, "levels_requested": 4, "policy": "fp32",
+            "parallelism": f"replicas x{args.gpus}" if args.gpus > 1 else "single GPU",
+            "l2": "working set > 126 MB L2 (L1 operator 258 MB); L2 also flushed before each timed solve"}
+
+
+def run_gpu(args):
+    import ctypes
+
+    import numpy as np
+    import torch
+
+    world, rank, local = _dist()
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import paper_2604_26441_b200 as P
+    from paper_2604_26441_b200 import _dev, _native
+
+    lib = _native.load()
+    N = args.size
+    g = P.build_cantilever(N, N, N)
+    op = P.FineOperator(g, P.simp_modulus(P.make_state("uniform", N, N, N, vf=0.5), 3.0))
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        h = P.build_hierarchy(op, 4, "fp32")
+    torch.cuda.synchronize()
+    setup_s = time.perf_counter() - t0
+    b_host = np.ascontiguousarray(g.load[g.free_dofs])
+    b_dev, _ = _dev.as_device(b_host)
+    cfg = P.SolverConfig(tol=1e-6, maxiter=200)
+    flush = torch.empty(256 * 2 ** 20 // 4, dtype=torch.float32, device="cuda")
+    stream = torch.cuda.current_stream()
+
+    for _ in range(args.warmup):
+        rep = P.pcg(op.matvec, h.vcycle, b_dev, cfg)
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    launches0 = lib.sg_launch_count()
+    total_ms = 0.0
+    iters = []
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            flush.zero_()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            rep = P.pcg(op.matvec, h.vcycle, b_dev, cfg)
+            e1.record(stream)
+            e1.synchronize()
+            total_ms += e0.elapsed_time(e1)
+            iters.append(rep.iterations)
+    launches = int(lib.sg_launch_count() - launches0)
+    torch.cuda.synchronize()
+    ms = total_ms / args.steps
+    if world > 1:
+        t = torch.tensor([ms], device="cuda", dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t.item())
+        torch.distributed.barrier()
+
+    # end to end through the public API: host b in, host x out
+    e2e = []
+    for k in range(max(3, min(args.steps, 5))):
+        flush.zero_()
+        torch.cuda.synchronize()
+        s = time.perf_counter()
+        rep_h = P.pcg(op.matvec, h.vcycle, b_host, cfg)
+        torch.cuda.synchronize()
+        e2e.append(time.perf_counter() - s)
+    e2e_s = sum(e2e) / len(e2e)
+
+    # per-component device timings (CUDA events inside the library)
+    def prof(what, reps=10):
+        out = ctypes.c_double()
+        _native.check(lib.sg_hier_profile(h._hh, what, reps, ctypes.byref(out), _dev.stream()))
+        return out.value
+
+    n_free, n_elem = g.n_free, g.n_elem
+    nn1 = (N // 2 + 1) ** 3
+    comps = {}
+    t32 = prof(0)
+    t64 = prof(1)
+    tl1 = prof(2)
+    tco = prof(3)
+    tvc = prof(4)
+    peak, peak_kind = _peaks()
+    b32 = 8 * n_free + 4 * n_elem
+    b64 = 16 * n_free + 8 * n_elem
+    bl1 = (243 * 8 + 48) * nn1
+    comps["fine_apply_fp32"] = {"ms": t32, "alg_bytes": b32, "gbs": b32 / t32 / 1e6}
+    comps["fine_apply_fp64"] = {"ms": t64, "alg_bytes": b64, "gbs": b64 / t64 / 1e6}
+    comps["level1_spmv_fp64"] = {"ms": tl1, "alg_bytes": bl1, "gbs": bl1 / tl1 / 1e6}
+    comps["coarsest_pcg80"] = {"ms": tco}
+    comps["vcycle"] = {"ms": tvc}
+    achieved = b32 / (t32 * 1e-3) / 1e9
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get("fine_apply_fp32_bytes")
+        except Exception:
+            traffic = None
+    line = {
+        "metric": METRIC, "value": ms / 1e3, "unit": "s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32 (fine level) / f64 (coarse, outer PCG)",
+        "data": "synthetic (uniform rho=0.5 cantilever, deterministic fixture)",
+        "config": _config(args),
+        "pcg_iters": iters[-1], "final_true_residual": rep.final_true_residual,
+        "converged": bool(rep.converged), "setup_s": setup_s,
+        "fine_matvec_gbs": achieved,
+        "roofline": {"kernel": "fine_apply_fp32 (fine_apply_kernel<float,1>)", "bound": "hbm",
+                     "achieved": achieved, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic,
+                     "alg_bytes_per_launch": b32, "launch_ms": t32},
+        "components": comps,
+        "e2e": {"value": e2e_s, "unit": "s", "h2d_bytes_per_step": 8 * n_free,
+                "d2h_bytes_per_step": 8 * n_free + 8 * (cfg.maxiter + 1)},
+        "gpu_launches": launches // max(args.steps, 1),
+        "clocks": clk.summary(),
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cb = oracle_iterations(N, steps=2, warmup=0)
+        line["cpu_baseline"] = {"value": cb["per_iter_s"] * iters[-1], "unit": "s",
+                                "cores": os.cpu_count(), "kind": "port",
+                                "sample": f"{cb['iters_timed']} oracle PCG iterations at {N}^3 "
+                                          f"(after a {cb['setup_s']:.1f}s oracle setup), scaled by "
+                                          f"{iters[-1]} iterations"}
+    if rank == 0:
+        print(json.dumps(line))
+    if world > 1:
+        torch.distributed.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="native", choices=["native", "reference"])
+    ap.add_argument("--size", type=int, default=100)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_gpu(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

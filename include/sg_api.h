@@ -48,6 +48,12 @@ void sg_fine_destroy(sg_fine* op);
 int64_t sg_fine_n_free(const sg_fine* op);
 /* FineOperator.matvec_tagged (fine_operator.py:56-77); tag SG_TAG_*. */
 int sg_fine_apply(sg_fine* op, int tag, const void* u_free, void* y_free, void* stream);
+/* Same apply on NODE-layout device vectors (3*(nx+1)*(ny+1)*(nz+1), Dirichlet
+ * entries zero): the raw kernel without the free<->node gather/scatter. */
+int sg_fine_apply_nodes(sg_fine* op, int tag, const void* u_nodes, void* y_nodes, void* stream);
+int64_t sg_fine_n_nodes(const sg_fine* op);
+/* Number of kernel launches issued by the library so far (instrumentation). */
+uint64_t sg_launch_count(void);
 /* FineOperator.diagonal (fine_operator.py:79-86), floored. */
 int sg_fine_diagonal(sg_fine* op, double* d_free, void* stream);
 /* FineOperator.assemble_dense (fine_operator.py:88-101): device n_free^2. */
@@ -119,6 +125,11 @@ int sg_hier_coarsest_solve(sg_hier* h, const double* r_free, double* x_free, voi
  * indices == NULL to get nnz in *nnz first. */
 int sg_hier_transfer_csr(sg_hier* h, int level, int64_t* indptr, int64_t* indices, double* data,
                          int64_t* nnz);
+
+/* Device time (ms, CUDA events, L2 flushed before each rep) of one hot-path
+ * component: 0 fine apply FP32, 1 fine apply FP64, 2 level-1 SpMV FP64,
+ * 3 coarsest solve, 4 full V-cycle, 5 fine apply BF16.  Bench instrumentation. */
+int sg_hier_profile(sg_hier* h, int what, int reps, double* ms_avg, void* stream);
 
 /* ---------------------------------------------------------------------
  * Standalone transfers and level-1 assembly (transfer.py)

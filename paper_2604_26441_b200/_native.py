@@ -52,6 +52,9 @@ SIGNATURES = {
     "sg_fine_destroy": (None, [c_void_p]),
     "sg_fine_n_free": (c_i64, [c_void_p]),
     "sg_fine_apply": (c_int, [c_void_p, c_int, c_void_p, c_void_p, c_void_p]),
+    "sg_fine_apply_nodes": (c_int, [c_void_p, c_int, c_void_p, c_void_p, c_void_p]),
+    "sg_fine_n_nodes": (c_i64, [c_void_p]),
+    "sg_launch_count": (c_u64, []),
     "sg_fine_diagonal": (c_int, [c_void_p, c_void_p, c_void_p]),
     "sg_fine_dense": (c_int, [c_void_p, c_void_p, c_void_p]),
     "sg_fine_boundary_codes": (c_int, [c_void_p, c_void_p, c_int, P(c_int)]),
@@ -69,6 +72,7 @@ SIGNATURES = {
     "sg_hier_prolong": (c_int, [c_void_p, c_int, c_void_p, c_void_p, c_void_p]),
     "sg_hier_restrict": (c_int, [c_void_p, c_int, c_void_p, c_void_p, c_void_p]),
     "sg_hier_coarsest_solve": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p]),
+    "sg_hier_profile": (c_int, [c_void_p, c_int, c_int, P(c_double), c_void_p]),
     "sg_hier_transfer_csr": (c_int, [c_void_p, c_int, c_void_p, c_void_p, c_void_p, P(c_i64)]),
     "sg_transfer_create": (c_int, [c_int, c_int, c_int, c_void_p, P(c_void_p)]),
     "sg_transfer_destroy": (None, [c_void_p]),

@@ -570,3 +570,70 @@ int sg_level1_csr(sg_fine* f, const double* triples, const uint32_t* codes, cons
 }
 
 }  // extern "C"
+
+namespace sg {
+unsigned long long g_sg_launches = 0;
+}
+
+extern "C" {
+
+uint64_t sg_launch_count(void) { return __atomic_load_n(&sg::g_sg_launches, __ATOMIC_RELAXED); }
+
+int sg_fine_apply_nodes(sg_fine* f, int tag, const void* u, void* y, void* stream) {
+  return guard([&] { sg::fine_apply_tag(f->op, tag, u, y, S(stream)); });
+}
+
+int64_t sg_fine_n_nodes(const sg_fine* f) { return f ? f->op.grid.d.nnodes() : -1; }
+
+}  // extern "C"
+
+// Per-kernel device timings for bench.py (CUDA events on the launch stream,
+// L2 flushed by a 256 MiB memset before every timed repetition).
+extern "C" int sg_hier_profile(sg_hier* h, int what, int reps, double* ms_avg, void* stream) {
+  return guard([&] {
+    std::lock_guard<std::mutex> lk(h->mu);
+    cudaStream_t s = S(stream);
+    sg::Hier& H = *h->h;
+    sg::Level& L0 = *H.lv[0];
+    const int64_t nd0 = L0.nd();
+    sg::DBuf<double> a(static_cast<size_t>(nd0)), b(static_cast<size_t>(nd0));
+    sg::DBuf<float> fa(static_cast<size_t>(nd0)), fb(static_cast<size_t>(nd0));
+    sg::DBuf<uint8_t> flush(size_t(256) << 20);
+    SG_CUDA(cudaMemsetAsync(a.p, 0, sizeof(double) * nd0, s));
+    SG_CUDA(cudaMemsetAsync(fa.p, 0, sizeof(float) * nd0, s));
+    cudaEvent_t e0, e1;
+    SG_CUDA(cudaEventCreate(&e0));
+    SG_CUDA(cudaEventCreate(&e1));
+    double total = 0.0;
+    for (int r = 0; r < reps; ++r) {
+      SG_CUDA(cudaMemsetAsync(flush.p, r & 0xff, flush.n, s));
+      SG_CUDA(cudaEventRecord(e0, s));
+      switch (what) {
+        case 0: sg::fine_apply_f32(*H.fine, fa.p, fb.p, s); break;
+        case 1: sg::fine_apply_f64(*H.fine, a.p, b.p, s); break;
+        case 2: {
+          SG_REQUIRE(H.lv.size() > 1, "no level 1");
+          sg::Level& L1 = *H.lv[1];
+          sg::stencil_apply<double>(*L1.g, L1.st.A64.p, L1.w.r.p, L1.w.y64.p, s);
+          break;
+        }
+        case 3: {
+          sg::Level& Lc = *H.lv.back();
+          sg::coarsest_solve(H, Lc.w.r.p, Lc.w.x.p, s);
+          break;
+        }
+        case 4: sg::cycle(H, 0, 1, s); break;
+        case 5: sg::fine_apply_bf16(*H.fine, fa.p, fb.p, s); break;
+        default: throw sg::Error("unknown profile target");
+      }
+      SG_CUDA(cudaEventRecord(e1, s));
+      SG_CUDA(cudaEventSynchronize(e1));
+      float ms = 0.f;
+      SG_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+      total += ms;
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    *ms_avg = total / std::max(reps, 1);
+  });
+}

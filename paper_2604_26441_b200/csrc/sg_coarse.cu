@@ -209,6 +209,7 @@ void Pcg80::solve(const double* b, double* x, cudaStream_t s) {
   a.steps = steps;
   void* args[] = {&a};
   SG_CUDA(cudaLaunchCooperativeKernel((void*)pcg80_kernel, dim3(nblocks), dim3(256), args, 0, s));
+  SG_CHECK_LAUNCH();
 }
 
 // ------------------------------------------------------------------ dense

@@ -28,7 +28,14 @@ struct Error : std::runtime_error {
                         " at " __FILE__ ":" + std::to_string(__LINE__));           \
   } while (0)
 
-#define SG_CHECK_LAUNCH() SG_CUDA(cudaGetLastError())
+// Every kernel launch of the library is followed by SG_CHECK_LAUNCH(), which
+// also counts it (sg_launch_count(): evidence of native launches per step).
+extern unsigned long long g_sg_launches;
+#define SG_CHECK_LAUNCH()                                 \
+  do {                                                    \
+    __atomic_add_fetch(&::sg::g_sg_launches, 1ull, __ATOMIC_RELAXED); \
+    SG_CUDA(cudaGetLastError());                          \
+  } while (0)
 
 #define SG_REQUIRE(cond, msg)                                                      \
   do {                                                                             \
