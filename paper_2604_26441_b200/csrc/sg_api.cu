@@ -83,6 +83,7 @@ int sg_fine_create(int nx, int ny, int nz, const uint8_t* dof_mask, const double
       f->op.ke16.k[q] = sg::bf16_round(float(ke[q]));
     }
     for (int q = 0; q < 24; ++q) f->op.kdiag.d[q] = ke[q * 24 + q];
+    f->op.walsh_ok = sg::walsh_params(ke, f->op.kw64, f->op.kw32);
     const size_t nd = size_t(3 * f->op.grid.d.nnodes());
     f->w.u64.alloc(nd);
     f->w.y64.alloc(nd);

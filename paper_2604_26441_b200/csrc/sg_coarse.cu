@@ -33,29 +33,34 @@ struct Pcg80Args {
   int steps;
 };
 
+// Every block sums the grid partials in the same fixed order (lane-strided
+// accumulation + fixed xor tree in warp 0): identical bits on all blocks.
 __device__ __forceinline__ double grid_total(const double* partials, int nb, double* sh) {
-  // every block sums the partials in index order: identical bits everywhere
-  __syncthreads();
-  if (threadIdx.x == 0) {
+  if (threadIdx.x < 32) {
     double s = 0.0;
-    for (int b = 0; b < nb; ++b) s = __dadd_rn(s, ((volatile const double*)partials)[b]);
-    *sh = s;
+    for (int b = threadIdx.x; b < nb; b += 32) s += __ldcg(partials + b);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (threadIdx.x == 0) *sh = s;
   }
   __syncthreads();
-  return *sh;
+  const double v = *sh;
+  __syncthreads();
+  return v;
 }
 
 __device__ __forceinline__ void block_partial(double v, double* out, double* sm) {
+#pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (lane == 0) sm[warp] = v;
   __syncthreads();
-  if (threadIdx.x == 0) {
-    double s = sm[0];
-    for (int w = 1; w < int(blockDim.x >> 5); ++w) s += sm[w];
-    *out = s;
+  if (threadIdx.x < 32) {
+    double s = threadIdx.x < (blockDim.x >> 5) ? sm[threadIdx.x] : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (threadIdx.x == 0) __stcg(out, s);
   }
-  __syncthreads();
 }
 
 __global__ void __launch_bounds__(256) pcg80_kernel(Pcg80Args P) {
@@ -63,6 +68,7 @@ __global__ void __launch_bounds__(256) pcg80_kernel(Pcg80Args P) {
   __shared__ double sm[8];
   __shared__ double tot;
   const int64_t nn = P.g.nnodes();
+  const int64_t nd = 3 * nn;
   const int NX = P.g.nx + 1, NY = P.g.ny + 1;
   const int64_t tid = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   const int64_t stride = int64_t(gridDim.x) * blockDim.x;
@@ -72,7 +78,7 @@ __global__ void __launch_bounds__(256) pcg80_kernel(Pcg80Args P) {
 
   // x = 0; r = b; z = dinv*r; p = z; rz = r.z
   double loc = 0.0;
-  for (int64_t d = tid; d < 3 * nn; d += stride) {
+  for (int64_t d = tid; d < nd; d += stride) {
     const double rv = P.b[d];
     const double zv = __dmul_rn(P.dinv[d], rv);
     P.x[d] = 0.0;
@@ -89,11 +95,17 @@ __global__ void __launch_bounds__(256) pcg80_kernel(Pcg80Args P) {
   for (int s = 0; s < P.steps; ++s) {
     const double* pold = (s & 1) ? P.p1 : P.p0;
     double* pnew = (s & 1) ? P.p0 : P.p1;
-    // phase A: p_new = z + beta*p_old (on the fly), q = K p_new + eps p_new, pq
+    // phase A (one thread per DOF row): p_new = z + beta*p_old recomputed for
+    // the neighbours, q = K p_new + eps p_new, partial p.q
     loc = 0.0;
-    for (int64_t node = tid; node < nn; node += stride) {
+    for (int64_t t = tid; t < nd; t += stride) {
+      // consecutive threads take consecutive nodes of one row component, so
+      // the SoA stencil loads of a warp are fully coalesced
+      const int ra = int(t / nn);
+      const int64_t node = t - int64_t(ra) * nn;
+      const int64_t d = 3 * node + ra;
       const int i = int(node % NX), j = int((node / NX) % NY), k = int(node / (int64_t(NX) * NY));
-      double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+      double acc = 0.0;
       for (int dk = -1; dk <= 1; ++dk) {
         if (k + dk < 0 || k + dk > P.g.nz) continue;
         for (int dj = -1; dj <= 1; ++dj) {
@@ -102,36 +114,21 @@ __global__ void __launch_bounds__(256) pcg80_kernel(Pcg80Args P) {
             if (i + di < 0 || i + di > P.g.nx) continue;
             const int slot = (dk + 1) * 9 + (dj + 1) * 3 + (di + 1);
             const int64_t m = node + di + int64_t(NX) * (dj + int64_t(NY) * dk);
-            double pv[3];
+            const double* a = P.A + (int64_t(slot) * 9 + ra * 3) * nn + node;
 #pragma unroll
-            for (int c = 0; c < 3; ++c)
-              pv[c] = have_beta ? __dadd_rn(P.z[3 * m + c], __dmul_rn(beta, pold[3 * m + c]))
-                                : pold[3 * m + c];
-            const double* a = P.A + int64_t(slot) * 9 * nn + node;
-            s0 = __dadd_rn(s0, __dmul_rn(a[0 * nn], pv[0]));
-            s0 = __dadd_rn(s0, __dmul_rn(a[1 * nn], pv[1]));
-            s0 = __dadd_rn(s0, __dmul_rn(a[2 * nn], pv[2]));
-            s1 = __dadd_rn(s1, __dmul_rn(a[3 * nn], pv[0]));
-            s1 = __dadd_rn(s1, __dmul_rn(a[4 * nn], pv[1]));
-            s1 = __dadd_rn(s1, __dmul_rn(a[5 * nn], pv[2]));
-            s2 = __dadd_rn(s2, __dmul_rn(a[6 * nn], pv[0]));
-            s2 = __dadd_rn(s2, __dmul_rn(a[7 * nn], pv[1]));
-            s2 = __dadd_rn(s2, __dmul_rn(a[8 * nn], pv[2]));
-            if (slot == 13) {
-#pragma unroll
-              for (int c = 0; c < 3; ++c) pnew[3 * node + c] = pv[c];
+            for (int c = 0; c < 3; ++c) {
+              const double pv = have_beta ? __dadd_rn(P.z[3 * m + c], __dmul_rn(beta, pold[3 * m + c]))
+                                          : pold[3 * m + c];
+              acc = __dadd_rn(acc, __dmul_rn(__ldg(a + c * nn), pv));
             }
           }
         }
       }
-      const double sv[3] = {s0, s1, s2};
-#pragma unroll
-      for (int c = 0; c < 3; ++c) {
-        const double pc = pnew[3 * node + c];
-        const double qv = __dadd_rn(sv[c], __dmul_rn(P.eps, pc));
-        P.q[3 * node + c] = qv;
-        loc += pc * qv;
-      }
+      const double pc = have_beta ? __dadd_rn(P.z[d], __dmul_rn(beta, pold[d])) : pold[d];
+      pnew[d] = pc;
+      const double qv = __dadd_rn(acc, __dmul_rn(P.eps, pc));
+      P.q[d] = qv;
+      loc += pc * qv;
     }
     block_partial(loc, &partA[blockIdx.x], sm);
     grid.sync();
@@ -140,7 +137,7 @@ __global__ void __launch_bounds__(256) pcg80_kernel(Pcg80Args P) {
     const double a = __ddiv_rn(rz, pq);
     // phase B: x += a p; r -= a q; z = dinv r; rz_new
     loc = 0.0;
-    for (int64_t d = tid; d < 3 * nn; d += stride) {
+    for (int64_t d = tid; d < nd; d += stride) {
       const double pv = pnew[d];
       P.x[d] = __dadd_rn(P.x[d], __dmul_rn(a, pv));
       const double rv = __dsub_rn(P.r[d], __dmul_rn(a, P.q[d]));
@@ -185,7 +182,7 @@ void Pcg80::setup(const Grid& g, const double* A, const double* diag, double eps
   SG_CUDA(cudaGetDevice(&dev));
   SG_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
   SG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pcg80_kernel, 256, 0));
-  const int64_t want = (g.d.nnodes() + 255) / 256;
+  const int64_t want = (3 * g.d.nnodes() + 255) / 256;
   int64_t cap = int64_t(nsm) * std::max(per_sm, 1);
   nblocks = int(std::max<int64_t>(1, std::min(want, cap)));
   partials.alloc(size_t(2 * nblocks));

@@ -101,11 +101,19 @@ static void launch_apply(const GridDesc& g, const uint8_t* nmask, const T* u, T*
   SG_CHECK_LAUNCH();
 }
 
-void fine_apply_f64(const FineOp& op, const double* u, double* y, cudaStream_t s) {
+void fine_apply_dense_f64(const FineOp& op, const double* u, double* y, cudaStream_t s) {
   launch_apply<double, 0>(op.grid.d, op.grid.nmask.p, u, y, op.E64.p, op.ke64, s);
 }
-void fine_apply_f32(const FineOp& op, const float* u, float* y, cudaStream_t s) {
+void fine_apply_dense_f32(const FineOp& op, const float* u, float* y, cudaStream_t s) {
   launch_apply<float, 1>(op.grid.d, op.grid.nmask.p, u, y, op.E32.p, op.ke32, s);
+}
+void fine_apply_f64(const FineOp& op, const double* u, double* y, cudaStream_t s) {
+  if (op.walsh_ok) fine_apply_walsh_f64(op, u, y, s);
+  else fine_apply_dense_f64(op, u, y, s);
+}
+void fine_apply_f32(const FineOp& op, const float* u, float* y, cudaStream_t s) {
+  if (op.walsh_ok) fine_apply_walsh_f32(op, u, y, s);
+  else fine_apply_dense_f32(op, u, y, s);
 }
 void fine_apply_bf16(const FineOp& op, const float* u, float* y, cudaStream_t s) {
   launch_apply<float, 2>(op.grid.d, op.grid.nmask.p, u, y, op.E32.p, op.ke16, s);

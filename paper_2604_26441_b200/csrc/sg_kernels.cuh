@@ -14,6 +14,12 @@ struct KeParam {
 struct KeDiag {
   double d[24];
 };
+// Nonzeros of (W Ke W)/64 in the tensor Walsh basis (sg_fine_walsh.cu)
+template <class T>
+struct KwParam {
+  T v[45];
+};
+bool walsh_params(const double* ke, KwParam<double>& p64, KwParam<float>& p32);
 
 // ---------------------------------------------------------------- fine level
 struct FineOp {
@@ -25,10 +31,19 @@ struct FineOp {
   KeParam<float> ke32;
   KeParam<float> ke16;  // bf16-rounded Ke32 (fine_operator.py:45)
   KeDiag kdiag;
+  KwParam<double> kw64;
+  KwParam<float> kw32;
+  bool walsh_ok = false;
   double emax = 0.0;
 };
 
+// FP64 / FP32 dispatch to the Walsh streaming kernel when the element matrix
+// has the 45-entry Walsh pattern, else the dense node-centric kernel.
 void fine_apply_f64(const FineOp& op, const double* u, double* y, cudaStream_t s);
+void fine_apply_walsh_f32(const FineOp& op, const float* u, float* y, cudaStream_t s);
+void fine_apply_walsh_f64(const FineOp& op, const double* u, double* y, cudaStream_t s);
+void fine_apply_dense_f32(const FineOp& op, const float* u, float* y, cudaStream_t s);
+void fine_apply_dense_f64(const FineOp& op, const double* u, double* y, cudaStream_t s);
 void fine_apply_f32(const FineOp& op, const float* u, float* y, cudaStream_t s);
 void fine_apply_bf16(const FineOp& op, const float* u, float* y, cudaStream_t s);
 void fine_diag_raw(const FineOp& op, double* d, cudaStream_t s);
