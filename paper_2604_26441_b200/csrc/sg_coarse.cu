@@ -9,11 +9,9 @@
 //    costs two grid barriers instead of three.
 //  * dense: Cholesky of K + eps*I computed on device at setup, then the
 //    explicit inverse, so each V-cycle's coarsest solve is one GEMV.
-#include <cooperative_groups.h>
 #include <cmath>
 #include "sg_coarse.cuh"
 
-namespace cg = cooperative_groups;
 
 namespace sg {
 
@@ -28,10 +26,26 @@ struct Pcg80Args {
   double* p0;
   double* p1;
   double* q;
-  double* partials;  // 2 * gridDim.x
+  double* partials;    // 2 * gridDim.x
+  unsigned* bar;       // monotonic arrival counter (zeroed before launch)
   double eps;
   int steps;
 };
+
+// Grid-wide barrier for a co-resident (cooperative) grid: one release-add per
+// block on a monotonic counter and an acquire spin; the L1 is invalidated by
+// the acquire so data written by other blocks before the barrier is seen.
+__device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned target) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(bar) : "memory");
+    unsigned v;
+    do {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(bar) : "memory");
+    } while (v < target);
+  }
+  __syncthreads();
+}
 
 // Every block sums the grid partials in the same fixed order (lane-strided
 // accumulation + fixed xor tree in warp 0): identical bits on all blocks.
@@ -63,10 +77,16 @@ __device__ __forceinline__ void block_partial(double v, double* out, double* sm)
   }
 }
 
-__global__ void __launch_bounds__(256) pcg80_kernel(Pcg80Args P) {
-  cg::grid_group grid = cg::this_grid();
-  __shared__ double sm[8];
+constexpr int kPcgNodes = 128;                 // nodes per block pass
+constexpr int kPcgThreads = 3 * kPcgNodes;     // one thread per (node, dk plane)
+
+// The reference pcg80 (hierarchy.py:139-162) as one persistent kernel.  Its
+// dot products are not bit-reproducible in the reference either (OpenBLAS
+// ddot), so the SpMV here uses FMA and three independent row accumulators.
+__global__ void __launch_bounds__(kPcgThreads) pcg80_kernel(Pcg80Args P) {
+  __shared__ double sm[kPcgThreads / 32];
   __shared__ double tot;
+  __shared__ double rowpart[2][kPcgNodes][3];
   const int64_t nn = P.g.nnodes();
   const int64_t nd = 3 * nn;
   const int NX = P.g.nx + 1, NY = P.g.ny + 1;
@@ -75,12 +95,13 @@ __global__ void __launch_bounds__(256) pcg80_kernel(Pcg80Args P) {
   const int nb = gridDim.x;
   double* partA = P.partials;
   double* partB = P.partials + nb;
+  unsigned epoch = 0;
 
   // x = 0; r = b; z = dinv*r; p = z; rz = r.z
   double loc = 0.0;
   for (int64_t d = tid; d < nd; d += stride) {
     const double rv = P.b[d];
-    const double zv = __dmul_rn(P.dinv[d], rv);
+    const double zv = P.dinv[d] * rv;
     P.x[d] = 0.0;
     P.r[d] = rv;
     P.z[d] = zv;
@@ -88,70 +109,95 @@ __global__ void __launch_bounds__(256) pcg80_kernel(Pcg80Args P) {
     loc += rv * zv;
   }
   block_partial(loc, &partB[blockIdx.x], sm);
-  grid.sync();
+  grid_barrier(P.bar, ++epoch * nb);
   double rz = grid_total(partB, nb, &tot);
   double beta = 0.0;
-  bool have_beta = false;
   for (int s = 0; s < P.steps; ++s) {
     const double* pold = (s & 1) ? P.p1 : P.p0;
     double* pnew = (s & 1) ? P.p0 : P.p1;
-    // phase A (one thread per DOF row): p_new = z + beta*p_old recomputed for
-    // the neighbours, q = K p_new + eps p_new, partial p.q
+    const bool hb = s > 0;
+    // phase A (one thread per node, 3 rows): p_new = z + beta*p_old recomputed
+    // for the 27 neighbours, q = K p_new + eps p_new, partial p.q
+    // Three threads per node (one per neighbour plane dk), 128 nodes per block
+    // pass: consecutive threads of a part take consecutive nodes, so the SoA
+    // stencil loads are coalesced; the three partial row sums meet in shared
+    // memory in a fixed order.
     loc = 0.0;
-    for (int64_t t = tid; t < nd; t += stride) {
-      // consecutive threads take consecutive nodes of one row component, so
-      // the SoA stencil loads of a warp are fully coalesced
-      const int ra = int(t / nn);
-      const int64_t node = t - int64_t(ra) * nn;
-      const int64_t d = 3 * node + ra;
-      const int i = int(node % NX), j = int((node / NX) % NY), k = int(node / (int64_t(NX) * NY));
-      double acc = 0.0;
-      for (int dk = -1; dk <= 1; ++dk) {
-        if (k + dk < 0 || k + dk > P.g.nz) continue;
-        for (int dj = -1; dj <= 1; ++dj) {
-          if (j + dj < 0 || j + dj > P.g.ny) continue;
-          for (int di = -1; di <= 1; ++di) {
-            if (i + di < 0 || i + di > P.g.nx) continue;
-            const int slot = (dk + 1) * 9 + (dj + 1) * 3 + (di + 1);
-            const int64_t m = node + di + int64_t(NX) * (dj + int64_t(NY) * dk);
-            const double* a = P.A + (int64_t(slot) * 9 + ra * 3) * nn + node;
+    const int part = threadIdx.x / kPcgNodes;
+    const int lnode = threadIdx.x % kPcgNodes;
+    for (int64_t base = int64_t(blockIdx.x) * kPcgNodes; base < nn; base += int64_t(gridDim.x) * kPcgNodes) {
+      const int64_t node = base + lnode;
+      double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+      if (node < nn) {
+        const int i = int(node % NX), j = int((node / NX) % NY), k = int(node / (int64_t(NX) * NY));
+        const int dk = part - 1;
+        if (k + dk >= 0 && k + dk <= P.g.nz) {
 #pragma unroll
-            for (int c = 0; c < 3; ++c) {
-              const double pv = have_beta ? __dadd_rn(P.z[3 * m + c], __dmul_rn(beta, pold[3 * m + c]))
-                                          : pold[3 * m + c];
-              acc = __dadd_rn(acc, __dmul_rn(__ldg(a + c * nn), pv));
-            }
+          for (int q9 = 0; q9 < 9; ++q9) {
+            const int di = q9 % 3 - 1, dj = q9 / 3 - 1;
+            if (i + di < 0 || i + di > P.g.nx || j + dj < 0 || j + dj > P.g.ny) continue;
+            const int slot = part * 9 + q9;
+            const int64_t m = node + di + int64_t(NX) * (dj + int64_t(NY) * dk);
+            const double* a = P.A + int64_t(slot) * 9 * nn + node;
+            double pv[3];
+#pragma unroll
+            for (int c = 0; c < 3; ++c)
+              pv[c] = hb ? fma(beta, pold[3 * m + c], P.z[3 * m + c]) : pold[3 * m + c];
+            a0 = fma(__ldg(a + 0 * nn), pv[0], a0);
+            a0 = fma(__ldg(a + 1 * nn), pv[1], a0);
+            a0 = fma(__ldg(a + 2 * nn), pv[2], a0);
+            a1 = fma(__ldg(a + 3 * nn), pv[0], a1);
+            a1 = fma(__ldg(a + 4 * nn), pv[1], a1);
+            a1 = fma(__ldg(a + 5 * nn), pv[2], a1);
+            a2 = fma(__ldg(a + 6 * nn), pv[0], a2);
+            a2 = fma(__ldg(a + 7 * nn), pv[1], a2);
+            a2 = fma(__ldg(a + 8 * nn), pv[2], a2);
           }
         }
       }
-      const double pc = have_beta ? __dadd_rn(P.z[d], __dmul_rn(beta, pold[d])) : pold[d];
-      pnew[d] = pc;
-      const double qv = __dadd_rn(acc, __dmul_rn(P.eps, pc));
-      P.q[d] = qv;
-      loc += pc * qv;
+      if (part > 0) {
+        rowpart[part - 1][lnode][0] = a0;
+        rowpart[part - 1][lnode][1] = a1;
+        rowpart[part - 1][lnode][2] = a2;
+      }
+      __syncthreads();
+      if (part == 0 && node < nn) {
+        const double av[3] = {a0 + rowpart[0][lnode][0] + rowpart[1][lnode][0],
+                              a1 + rowpart[0][lnode][1] + rowpart[1][lnode][1],
+                              a2 + rowpart[0][lnode][2] + rowpart[1][lnode][2]};
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          const int64_t d = 3 * node + c;
+          const double pc = hb ? fma(beta, pold[d], P.z[d]) : pold[d];
+          pnew[d] = pc;
+          const double qv = fma(P.eps, pc, av[c]);
+          P.q[d] = qv;
+          loc = fma(pc, qv, loc);
+        }
+      }
+      __syncthreads();
     }
     block_partial(loc, &partA[blockIdx.x], sm);
-    grid.sync();
+    grid_barrier(P.bar, ++epoch * nb);
     const double pq = grid_total(partA, nb, &tot);
     if (!(pq > 0.0) || !isfinite(pq)) break;
-    const double a = __ddiv_rn(rz, pq);
+    const double a = rz / pq;
     // phase B: x += a p; r -= a q; z = dinv r; rz_new
     loc = 0.0;
     for (int64_t d = tid; d < nd; d += stride) {
       const double pv = pnew[d];
-      P.x[d] = __dadd_rn(P.x[d], __dmul_rn(a, pv));
-      const double rv = __dsub_rn(P.r[d], __dmul_rn(a, P.q[d]));
+      P.x[d] = fma(a, pv, P.x[d]);
+      const double rv = fma(-a, P.q[d], P.r[d]);
       P.r[d] = rv;
-      const double zv = __dmul_rn(P.dinv[d], rv);
+      const double zv = P.dinv[d] * rv;
       P.z[d] = zv;
-      loc += rv * zv;
+      loc = fma(rv, zv, loc);
     }
     block_partial(loc, &partB[blockIdx.x], sm);
-    grid.sync();
+    grid_barrier(P.bar, ++epoch * nb);
     const double rzn = grid_total(partB, nb, &tot);
     if (!(rzn > 0.0) || !isfinite(rzn)) break;
-    beta = __ddiv_rn(rzn, rz);
-    have_beta = true;
+    beta = rzn / rz;
     rz = rzn;
   }
 }
@@ -169,11 +215,11 @@ void Pcg80::setup(const Grid& g, const double* A, const double* diag, double eps
   p0.alloc(size_t(nd));
   p1.alloc(size_t(nd));
   q.alloc(size_t(nd));
-  std::vector<double> h(static_cast<size_t>(size_t(nd)));
+  std::vector<double> h(static_cast<size_t>(nd));
   SG_CUDA(cudaMemcpyAsync(h.data(), diag, sizeof(double) * nd, cudaMemcpyDeviceToHost, s));
   SG_CUDA(cudaStreamSynchronize(s));
-  std::vector<uint8_t> fixed(size_t(nd), 1);
-  std::vector<int32_t> f2d(static_cast<size_t>(size_t(g.n_free)));
+  std::vector<uint8_t> fixed(static_cast<size_t>(nd), 1);
+  std::vector<int32_t> f2d(static_cast<size_t>(g.n_free));
   SG_CUDA(cudaMemcpy(f2d.data(), g.free2dof.p, sizeof(int32_t) * g.n_free, cudaMemcpyDeviceToHost));
   for (int32_t d : f2d) fixed[size_t(d)] = 0;
   for (int64_t d = 0; d < nd; ++d) h[size_t(d)] = fixed[size_t(d)] ? 0.0 : 1.0 / (h[size_t(d)] + eps);
@@ -181,11 +227,13 @@ void Pcg80::setup(const Grid& g, const double* A, const double* diag, double eps
   int dev = 0, nsm = 0, per_sm = 0;
   SG_CUDA(cudaGetDevice(&dev));
   SG_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-  SG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pcg80_kernel, 256, 0));
-  const int64_t want = (3 * g.d.nnodes() + 255) / 256;
-  int64_t cap = int64_t(nsm) * std::max(per_sm, 1);
+  SG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pcg80_kernel, kPcgThreads, 0));
+  const int64_t want = (g.d.nnodes() + kPcgNodes - 1) / kPcgNodes;
+  // one block per SM at most: the barrier cost grows with the participant count
+  const int64_t cap = int64_t(nsm) * std::min(std::max(per_sm, 1), 1);
   nblocks = int(std::max<int64_t>(1, std::min(want, cap)));
   partials.alloc(size_t(2 * nblocks));
+  bar.alloc(1);
   SG_CUDA(cudaStreamSynchronize(s));
 }
 
@@ -202,10 +250,13 @@ void Pcg80::solve(const double* b, double* x, cudaStream_t s) {
   a.p1 = p1.p;
   a.q = q.p;
   a.partials = partials.p;
+  a.bar = bar.p;
   a.eps = eps;
   a.steps = steps;
+  SG_CUDA(cudaMemsetAsync(bar.p, 0, sizeof(unsigned), s));
   void* args[] = {&a};
-  SG_CUDA(cudaLaunchCooperativeKernel((void*)pcg80_kernel, dim3(nblocks), dim3(256), args, 0, s));
+  SG_CUDA(cudaLaunchCooperativeKernel((void*)pcg80_kernel, dim3(nblocks), dim3(kPcgThreads), args,
+                                      0, s));
   SG_CHECK_LAUNCH();
 }
 

@@ -12,6 +12,7 @@ struct Pcg80 {
   int steps = 80;
   int nblocks = 0;
   DBuf<double> dinv, r, z, p0, p1, q, partials;
+  DBuf<unsigned> bar;
   void setup(const Grid& g, const double* A, const double* diag, double eps, int steps,
              cudaStream_t s);
   void solve(const double* b, double* x, cudaStream_t s);

@@ -84,7 +84,7 @@ constexpr int kWY = 16;   // element columns per tile along y (15 owned nodes)
 constexpr int kWThreads = kWX * kWY;
 
 template <class T>
-__global__ void __launch_bounds__(kWThreads, sizeof(T) == 4 ? 3 : 1)
+__global__ void __launch_bounds__(kWThreads, sizeof(T) == 4 ? 2 : 1)
 fine_apply_walsh_kernel(GridDesc g, const uint8_t* __restrict__ nmask, const T* __restrict__ u,
                         T* __restrict__ y, const T* __restrict__ E, KwParam<T> P, int kchunk) {
   __shared__ T ex[2][kWY][kWX][6];
@@ -101,16 +101,22 @@ fine_apply_walsh_kernel(GridDesc g, const uint8_t* __restrict__ nmask, const T* 
   // Corner loads use clamped (always valid) addresses: a corner is only ever
   // out of the domain for an element that is itself outside, and those get
   // modulus 0, so their (finite) inputs never reach a result.  No per-load
-  // predicates, one pointer bump per plane.
+  // predicates; running pointers advance one node plane per layer.
   const int ci0 = min(max(ei, 0), g.nx), ci1 = min(max(ei + 1, 0), g.nx);
   const int cj0 = min(max(ej, 0), g.ny), cj1 = min(max(ej + 1, 0), g.ny);
   const int off1 = 3 * (ci1 - ci0), off2 = 3 * NX * (cj1 - cj0);
   const int64_t plane = 3 * int64_t(NX) * NY;
   const T* ucol = u + 3 * (int64_t(ci0) + int64_t(NX) * cj0);
+  const T* ulast = ucol + int64_t(g.nz) * plane;
   const int64_t estride = int64_t(g.nx) * g.ny;
   const T* ecol = E + (col_in ? ei + int64_t(g.nx) * ej : 0);
-  auto load_plane = [&](int kp, T* dst) {
-    const T* p = ucol + int64_t(min(max(kp, 0), g.nz)) * plane;
+  // per-thread constants of the owned node column
+  const bool xface_fixed = g.xface && ni == 0;
+  T* yp = y + 3 * (int64_t(min(ni, g.nx)) + int64_t(NX) * min(nj, g.ny)) + int64_t(k0) * plane;
+  const uint8_t* mp = nmask ? nmask + (int64_t(min(ni, g.nx)) + int64_t(NX) * min(nj, g.ny)) +
+                                  int64_t(k0) * NX * NY : nullptr;
+
+  auto load_plane = [&](const T* p, T* dst) {
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
       dst[c] = __ldg(p + c);
@@ -124,34 +130,32 @@ fine_apply_walsh_kernel(GridDesc g, const uint8_t* __restrict__ nmask, const T* 
     const T e = __ldg(ecol + int64_t(min(max(ek, 0), g.nz - 1)) * estride);
     return el_ok ? e : T(0);
   };
+  const T* pnext = ucol + int64_t(max(k0 - 1, 0)) * plane;
 
-  T lo[12];  // u at the lower node plane of the current layer (corners 0..3)
-  load_plane(k0 - 1, lo);
   T carry[3] = {T(0), T(0), T(0)};
   int buf = 0;
-  // software pipeline: the upper plane of layer ek and its modulus are loaded
-  // one iteration ahead, so the global-load latency overlaps the element math
-  T hi[12];
-  T s_next;
-  load_plane(k0, hi);
-  s_next = load_E(k0 - 1);
-  for (int ek = k0 - 1; ek < k1; ++ek) {
+
+  // one element layer: lo = plane ek, hi = plane ek+1 (corners 0..3 each)
+  auto layer = [&](int ek, const T* lo, const T* hi, T s) {
     T v[24];
+    // forward Walsh on the 2x2x2 corners, built from lo/hi without copies
 #pragma unroll
-    for (int q = 0; q < 12; ++q) {
-      v[(q / 3) * 3 + q % 3] = lo[q];
-      v[12 + q] = hi[q];
-      lo[q] = hi[q];
+    for (int c = 0; c < 3; ++c) {
+      const T a0 = lo[c], a1 = lo[3 + c], a2 = lo[6 + c], a3 = lo[9 + c];
+      const T a4 = hi[c], a5 = hi[3 + c], a6 = hi[6 + c], a7 = hi[9 + c];
+      const T b0 = a0 + a1, b1 = a0 - a1, b2 = a2 + a3, b3 = a2 - a3;
+      const T b4 = a4 + a5, b5 = a4 - a5, b6 = a6 + a7, b7 = a6 - a7;
+      const T c0 = b0 + b2, c2 = b0 - b2, c1 = b1 + b3, c3 = b1 - b3;
+      const T c4 = b4 + b6, c6 = b4 - b6, c5 = b5 + b7, c7 = b5 - b7;
+      v[c] = T(0);  // constant mode: rigid translation, no energy
+      v[3 + c] = c1 + c5;
+      v[6 + c] = c2 + c6;
+      v[9 + c] = c3 + c7;
+      v[12 + c] = c0 - c4;
+      v[15 + c] = c1 - c5;
+      v[18 + c] = c2 - c6;
+      v[21 + c] = c3 - c7;
     }
-    const T s = s_next;
-    if (ek + 1 < k1) {
-      load_plane(ek + 2, hi);
-      s_next = load_E(ek + 1);
-    }
-    // forward Walsh per component
-#pragma unroll
-    for (int c = 0; c < 3; ++c) fwht8(v + c);
-    // sparse core: w = s * Kw v  (constant modes 0..2 stay zero)
     T w[24];
 #pragma unroll
     for (int r = 0; r < 24; ++r) w[r] = T(0);
@@ -159,7 +163,6 @@ fine_apply_walsh_kernel(GridDesc g, const uint8_t* __restrict__ nmask, const T* 
     for (int q = 0; q < 45; ++q) w[kKwRow[q]] += P.v[q] * v[kKwCol[q]];
 #pragma unroll
     for (int r = 3; r < 24; ++r) w[r] *= s;
-    // inverse Walsh per component -> 8 corner results
 #pragma unroll
     for (int c = 0; c < 3; ++c) fwht8(w + c);
     // x-combine: node (ei+1, ej+jy, ek+kz) <- own corner (1,jy,kz) + right corner (0,jy,kz)
@@ -175,28 +178,51 @@ fine_apply_walsh_kernel(GridDesc g, const uint8_t* __restrict__ nmask, const T* 
         }
     // y-combine through shared memory: node row ej+1 <- own jy=1 + upper thread's jy=0
 #pragma unroll
-    for (int t = 0; t < 6; ++t) ex[buf][ty][tx][t] = A[t];  // jy = 0 entries (kz, c)
+    for (int t = 0; t < 6; ++t) ex[buf][ty][tx][t] = A[t];
     __syncthreads();
     T B[6];
-    if (ty < kWY - 1) {
+    const bool up = ty < kWY - 1;
 #pragma unroll
-      for (int t = 0; t < 6; ++t) B[t] = A[6 + t] + ex[buf][ty + 1][tx][t];
-    } else {
-#pragma unroll
-      for (int t = 0; t < 6; ++t) B[t] = A[6 + t];
-    }
+    for (int t = 0; t < 6; ++t) B[t] = up ? A[6 + t] + ex[buf][ty + 1][tx][t] : A[6 + t];
     buf ^= 1;
     // z-combine: node plane ek = carry (top of layer ek-1) + bottom of layer ek
-    if (ek >= k0 && own) {
-      const int64_t node = ni + int64_t(NX) * (nj + int64_t(NY) * ek);
+    if (ek >= k0) {
+      if (own) {
 #pragma unroll
-      for (int c = 0; c < 3; ++c) {
-        const T val = carry[c] + B[c];
-        y[3 * node + c] = node_fixed_axis(g, nmask, node, ni, c) ? T(0) : val;
+        for (int c = 0; c < 3; ++c) {
+          const bool fixed = g.xface ? xface_fixed : ((mp[0] >> c) & 1);
+          yp[c] = fixed ? T(0) : carry[c] + B[c];
+        }
       }
+      yp += plane;
+      if (!g.xface) mp += int64_t(NX) * NY;
     }
 #pragma unroll
     for (int c = 0; c < 3; ++c) carry[c] = B[3 + c];
+  };
+
+  // three rotating plane buffers: the plane two layers ahead is in flight
+  // while the current element is computed
+  T QA[12], QB[12], QC[12];
+  load_plane(pnext, QA);  // plane k0-1 (clamped)
+  pnext = ucol + int64_t(min(max(k0, 0), g.nz)) * plane;
+  load_plane(pnext, QB);  // plane k0
+  T sA = load_E(k0 - 1);
+  for (int ek = k0 - 1; ek < k1; ek += 3) {
+    pnext = pnext < ulast ? pnext + plane : ulast;
+    load_plane(pnext, QC);
+    T sB = load_E(ek + 1);
+    layer(ek, QA, QB, sA);
+    if (ek + 1 >= k1) break;
+    pnext = pnext < ulast ? pnext + plane : ulast;
+    load_plane(pnext, QA);
+    T sC = load_E(ek + 2);
+    layer(ek + 1, QB, QC, sB);
+    if (ek + 2 >= k1) break;
+    pnext = pnext < ulast ? pnext + plane : ulast;
+    load_plane(pnext, QB);
+    sA = load_E(ek + 3);
+    layer(ek + 2, QC, QA, sC);
   }
 }
 
@@ -207,11 +233,20 @@ static void launch_walsh(const FineOp& op, const T* u, T* y, const T* E, const K
   const int tx = (g.nx + 1 + kWX - 2) / (kWX - 1);
   const int ty = (g.ny + 1 + kWY - 2) / (kWY - 1);
   const int planes = g.nz + 1;
-  // about two CTAs per SM in total, chunks of at least 8 planes
-  int nchunk = (2 * kNumSMs + tx * ty - 1) / (tx * ty);
-  nchunk = std::max(1, std::min(nchunk, (planes + 7) / 8));
-  const int kchunk = (planes + nchunk - 1) / nchunk;
-  nchunk = (planes + kchunk - 1) / kchunk;
+  // z-chunking: minimise the busiest SM's layer count, (CTAs per SM) x
+  // (layers per chunk incl. the halo layer), at two resident CTAs per SM
+  int best = 1, best_cost = 1 << 30;
+  for (int nc = 1; nc <= std::max(1, planes / 4); ++nc) {
+    const int kc = (planes + nc - 1) / nc;
+    const int n = (planes + kc - 1) / kc;
+    const int ctas = tx * ty * n;
+    const int waves = (ctas + 2 * kNumSMs - 1) / (2 * kNumSMs);
+    const int per_sm = (ctas + kNumSMs - 1) / kNumSMs;
+    const int cost = std::max(per_sm, 2 * waves) * (kc + 1);
+    if (cost < best_cost) { best_cost = cost; best = n; }
+  }
+  const int kchunk = (planes + best - 1) / best;
+  const int nchunk = (planes + kchunk - 1) / kchunk;
   dim3 grid(tx, ty, nchunk);
   fine_apply_walsh_kernel<T><<<grid, kWThreads, 0, s>>>(g, op.grid.nmask.p, u, y, E, P, kchunk);
   SG_CHECK_LAUNCH();
