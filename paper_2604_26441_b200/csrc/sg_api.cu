@@ -638,3 +638,23 @@ extern "C" int sg_hier_profile(sg_hier* h, int what, int reps, double* ms_avg, v
     *ms_avg = total / std::max(reps, 1);
   });
 }
+
+// Development instrumentation: %globaltimer stamps (ns) of block 0 in pcg80
+// step 10 at its phase boundaries (phase A, partial, barrier, total, phase B,
+// partial, barrier, total).  out: 9 int64.
+extern "C" int sg_hier_pcg80_trace(sg_hier* h, long long* out, void* stream) {
+  return guard([&] {
+    std::lock_guard<std::mutex> lk(h->mu);
+    cudaStream_t s = S(stream);
+    sg::Hier& H = *h->h;
+    SG_REQUIRE(H.coarsest_mode == 1, "coarsest solver is not pcg80");
+    sg::DBuf<long long> t(16);
+    t.zero(s);
+    sg::Level& Lc = *H.lv.back();
+    H.pcg.trace = t.p;
+    sg::coarsest_solve(H, Lc.w.r.p, Lc.w.x.p, s);
+    H.pcg.trace = nullptr;
+    t.download(out, 9, s);
+    SG_CUDA(cudaStreamSynchronize(s));
+  });
+}

@@ -2,16 +2,17 @@
 //
 //  * pcg80: the reference's fixed-count Jacobi-PCG on K + eps*I
 //    (_fixed_jacobi_pcg, hierarchy.py:139-162) as ONE persistent cooperative
-//    kernel: the 80 dependent steps never return to the host, dot products
-//    are reduced deterministically across the grid (fixed partial order),
-//    and the search-direction update is folded into the next SpMV (p is
-//    double-buffered and recomputed for neighbours on the fly) so each step
-//    costs two grid barriers instead of three.
+//    kernel (one block per SM): the 80 dependent steps never return to the
+//    host.  Each block keeps its operator rows resident in shared memory for
+//    the whole solve; per step: phase A (q = (K+eps I) p with p = z + beta
+//    p_old recomputed for the neighbours on the fly, branch-free), a grid
+//    all-reduce (tree barrier + every block summing the block partials in
+//    index order: deterministic), phase B (x, r, z updates) and a second
+//    all-reduce.
 //  * dense: Cholesky of K + eps*I computed on device at setup, then the
 //    explicit inverse, so each V-cycle's coarsest solve is one GEMV.
 #include <cmath>
 #include "sg_coarse.cuh"
-
 
 namespace sg {
 
@@ -26,76 +27,97 @@ struct Pcg80Args {
   double* p0;
   double* p1;
   double* q;
-  double* partials;    // 2 * gridDim.x
-  unsigned* bar;       // monotonic arrival counter (zeroed before launch)
+  double* partials;    // 2 * gridDim.x (double-buffered by epoch parity)
+  unsigned* bar;       // [0] root counter, [32] release flag, [64*(1+g)] group counters
   double eps;
   int steps;
+  int cache_slots;     // stencil slots resident in shared memory (single-pass grids)
+  long long* trace;    // optional: %globaltimer stamps of block 0, step 10
 };
 
-// Grid-wide barrier for a co-resident (cooperative) grid: one release-add per
-// block on a monotonic counter and an acquire spin; the L1 is invalidated by
-// the acquire so data written by other blocks before the barrier is seen.
-__device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned target) {
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(bar) : "memory");
-    unsigned v;
-    do {
-      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(bar) : "memory");
-    } while (v < target);
-  }
-  __syncthreads();
+#define PCG_STAMP(k)                                                                  \
+  do {                                                                                \
+    if (P.trace && s == 10 && blockIdx.x == 0 && threadIdx.x == 0) {                  \
+      long long t_;                                                                   \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                          \
+      P.trace[k] = t_;                                                                \
+    }                                                                                 \
+  } while (0)
+
+constexpr int kPcgNodes = 128;                 // nodes per block pass
+constexpr int kPcgThreads = 3 * kPcgNodes;     // one thread per (node, dk plane)
+constexpr int kBarGroup = 16;                  // blocks per first-level barrier group
+
+// Two-level arrival tree (groups of 16 blocks, then the group leaders) so no
+// counter sees more than 16-way atomic contention; the root releases a flag
+// that every block acquires.
+__device__ __forceinline__ void tree_barrier(unsigned* bar, unsigned epoch) {
+  // (measured: a flat monotonic counter beats both a 16-ary arrival tree and
+  // per-block flag polling on B200 at ~140 participants)
+  const unsigned target = epoch * gridDim.x;
+  asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(bar) : "memory");
+  unsigned f;
+  do {
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(f) : "l"(bar) : "memory");
+  } while (f < target);
 }
 
-// Every block sums the grid partials in the same fixed order (lane-strided
-// accumulation + fixed xor tree in warp 0): identical bits on all blocks.
-__device__ __forceinline__ double grid_total(const double* partials, int nb, double* sh) {
-  if (threadIdx.x < 32) {
-    double s = 0.0;
-    for (int b = threadIdx.x; b < nb; b += 32) s += __ldcg(partials + b);
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    if (threadIdx.x == 0) *sh = s;
-  }
-  __syncthreads();
-  const double v = *sh;
-  __syncthreads();
-  return v;
-}
-
-__device__ __forceinline__ void block_partial(double v, double* out, double* sm) {
+// Block partial (fixed shuffle tree + fixed warp order) -> partials; tree
+// barrier; every block sums all partials in index order (lane-strided +
+// fixed xor tree): identical totals on every block, deterministic.
+__device__ __forceinline__ double grid_allreduce(double v, const Pcg80Args& P, unsigned epoch,
+                                                 double* sm) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (lane == 0) sm[warp] = v;
   __syncthreads();
+  const int nb = gridDim.x;
+  double* part = P.partials + (epoch & 1) * nb;
   if (threadIdx.x < 32) {
-    double s = threadIdx.x < (blockDim.x >> 5) ? sm[threadIdx.x] : 0.0;
+    double s = lane < int(blockDim.x >> 5) ? sm[lane] : 0.0;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    if (threadIdx.x == 0) __stcg(out, s);
+    if (lane == 0) {
+      __stcg(part + blockIdx.x, s);
+      tree_barrier(P.bar, epoch);
+    }
+    __syncwarp();
+    double t = 0.0;
+    for (int b = lane; b < nb; b += 32) t += __ldcg(part + b);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+    if (lane == 0) sm[0] = t;
   }
+  __syncthreads();
+  const double tot = sm[0];
+  __syncthreads();
+  return tot;
 }
 
-constexpr int kPcgNodes = 128;                 // nodes per block pass
-constexpr int kPcgThreads = 3 * kPcgNodes;     // one thread per (node, dk plane)
-
-// The reference pcg80 (hierarchy.py:139-162) as one persistent kernel.  Its
-// dot products are not bit-reproducible in the reference either (OpenBLAS
-// ddot), so the SpMV here uses FMA and three independent row accumulators.
+// The reference pcg80 (hierarchy.py:139-162).  Its dot products are not
+// bit-reproducible in the reference either (OpenBLAS ddot), so the SpMV here
+// uses FMA and independent row accumulators; reductions are deterministic.
 __global__ void __launch_bounds__(kPcgThreads) pcg80_kernel(Pcg80Args P) {
   __shared__ double sm[kPcgThreads / 32];
-  __shared__ double tot;
   __shared__ double rowpart[2][kPcgNodes][3];
+  extern __shared__ double smA[];  // [cache_slots*9][kPcgNodes] operator rows of this block
   const int64_t nn = P.g.nnodes();
   const int64_t nd = 3 * nn;
   const int NX = P.g.nx + 1, NY = P.g.ny + 1;
   const int64_t tid = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   const int64_t stride = int64_t(gridDim.x) * blockDim.x;
-  const int nb = gridDim.x;
-  double* partA = P.partials;
-  double* partB = P.partials + nb;
   unsigned epoch = 0;
+  if (P.cache_slots > 0) {
+    const int64_t n0 = int64_t(blockIdx.x) * kPcgNodes;
+    const int total = P.cache_slots * 9 * kPcgNodes;
+    for (int idx = threadIdx.x; idx < total; idx += blockDim.x) {
+      const int t = idx / kPcgNodes, ln = idx % kPcgNodes;
+      const int64_t node = n0 + ln;
+      smA[idx] = node < nn ? __ldg(P.A + int64_t(t) * nn + node) : 0.0;
+    }
+    __syncthreads();
+  }
 
   // x = 0; r = b; z = dinv*r; p = z; rz = r.z
   double loc = 0.0;
@@ -108,52 +130,49 @@ __global__ void __launch_bounds__(kPcgThreads) pcg80_kernel(Pcg80Args P) {
     P.p0[d] = zv;
     loc += rv * zv;
   }
-  block_partial(loc, &partB[blockIdx.x], sm);
-  grid_barrier(P.bar, ++epoch * nb);
-  double rz = grid_total(partB, nb, &tot);
+  double rz = grid_allreduce(loc, P, ++epoch, sm);
   double beta = 0.0;
+  const int part = threadIdx.x / kPcgNodes;  // neighbour plane dk = part - 1
+  const int lnode = threadIdx.x % kPcgNodes;
   for (int s = 0; s < P.steps; ++s) {
     const double* pold = (s & 1) ? P.p1 : P.p0;
     double* pnew = (s & 1) ? P.p0 : P.p1;
     const bool hb = s > 0;
-    // phase A (one thread per node, 3 rows): p_new = z + beta*p_old recomputed
-    // for the 27 neighbours, q = K p_new + eps p_new, partial p.q
-    // Three threads per node (one per neighbour plane dk), 128 nodes per block
-    // pass: consecutive threads of a part take consecutive nodes, so the SoA
-    // stencil loads are coalesced; the three partial row sums meet in shared
-    // memory in a fixed order.
+    PCG_STAMP(0);
+    // phase A: q = (K + eps I) p_new, p_new = z + beta p_old
     loc = 0.0;
-    const int part = threadIdx.x / kPcgNodes;
-    const int lnode = threadIdx.x % kPcgNodes;
     for (int64_t base = int64_t(blockIdx.x) * kPcgNodes; base < nn; base += int64_t(gridDim.x) * kPcgNodes) {
       const int64_t node = base + lnode;
+      const int64_t cn = node < nn ? node : nn - 1;
+      const int i = int(cn % NX), j = int((cn / NX) % NY), k = int(cn / (int64_t(NX) * NY));
+      const int kk = min(max(k + part - 1, 0), P.g.nz);
       double a0 = 0.0, a1 = 0.0, a2 = 0.0;
-      if (node < nn) {
-        const int i = int(node % NX), j = int((node / NX) % NY), k = int(node / (int64_t(NX) * NY));
-        const int dk = part - 1;
-        if (k + dk >= 0 && k + dk <= P.g.nz) {
+      // branch-free: out-of-grid neighbours are clamped onto valid nodes;
+      // their stencil entries are stored as exact zeros.
 #pragma unroll
-          for (int q9 = 0; q9 < 9; ++q9) {
-            const int di = q9 % 3 - 1, dj = q9 / 3 - 1;
-            if (i + di < 0 || i + di > P.g.nx || j + dj < 0 || j + dj > P.g.ny) continue;
-            const int slot = part * 9 + q9;
-            const int64_t m = node + di + int64_t(NX) * (dj + int64_t(NY) * dk);
-            const double* a = P.A + int64_t(slot) * 9 * nn + node;
-            double pv[3];
+      for (int q9 = 0; q9 < 9; ++q9) {
+        const int ii = min(max(i + q9 % 3 - 1, 0), P.g.nx);
+        const int jj = min(max(j + q9 / 3 - 1, 0), P.g.ny);
+        const int64_t m = ii + int64_t(NX) * (jj + int64_t(NY) * kk);
+        const int slot = part * 9 + q9;
+        const bool cached = slot < P.cache_slots;
+        const double* a = cached ? smA + slot * 9 * kPcgNodes + lnode : P.A + int64_t(slot) * 9 * nn + cn;
+        const int64_t st = cached ? kPcgNodes : nn;
+        double pv[3];
 #pragma unroll
-            for (int c = 0; c < 3; ++c)
-              pv[c] = hb ? fma(beta, pold[3 * m + c], P.z[3 * m + c]) : pold[3 * m + c];
-            a0 = fma(__ldg(a + 0 * nn), pv[0], a0);
-            a0 = fma(__ldg(a + 1 * nn), pv[1], a0);
-            a0 = fma(__ldg(a + 2 * nn), pv[2], a0);
-            a1 = fma(__ldg(a + 3 * nn), pv[0], a1);
-            a1 = fma(__ldg(a + 4 * nn), pv[1], a1);
-            a1 = fma(__ldg(a + 5 * nn), pv[2], a1);
-            a2 = fma(__ldg(a + 6 * nn), pv[0], a2);
-            a2 = fma(__ldg(a + 7 * nn), pv[1], a2);
-            a2 = fma(__ldg(a + 8 * nn), pv[2], a2);
-          }
-        }
+        for (int c = 0; c < 3; ++c)
+          // plain (L1-cacheable) loads: the barrier's acquire invalidated the
+          // L1, and each neighbour value is reused by up to 27 rows of the block
+          pv[c] = hb ? fma(beta, pold[3 * m + c], P.z[3 * m + c]) : pold[3 * m + c];
+        a0 = fma(a[0 * st], pv[0], a0);
+        a0 = fma(a[1 * st], pv[1], a0);
+        a0 = fma(a[2 * st], pv[2], a0);
+        a1 = fma(a[3 * st], pv[0], a1);
+        a1 = fma(a[4 * st], pv[1], a1);
+        a1 = fma(a[5 * st], pv[2], a1);
+        a2 = fma(a[6 * st], pv[0], a2);
+        a2 = fma(a[7 * st], pv[1], a2);
+        a2 = fma(a[8 * st], pv[2], a2);
       }
       if (part > 0) {
         rowpart[part - 1][lnode][0] = a0;
@@ -168,7 +187,7 @@ __global__ void __launch_bounds__(kPcgThreads) pcg80_kernel(Pcg80Args P) {
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
           const int64_t d = 3 * node + c;
-          const double pc = hb ? fma(beta, pold[d], P.z[d]) : pold[d];
+          const double pc = hb ? fma(beta, __ldcg(pold + d), __ldcg(P.z + d)) : __ldcg(pold + d);
           pnew[d] = pc;
           const double qv = fma(P.eps, pc, av[c]);
           P.q[d] = qv;
@@ -177,25 +196,25 @@ __global__ void __launch_bounds__(kPcgThreads) pcg80_kernel(Pcg80Args P) {
       }
       __syncthreads();
     }
-    block_partial(loc, &partA[blockIdx.x], sm);
-    grid_barrier(P.bar, ++epoch * nb);
-    const double pq = grid_total(partA, nb, &tot);
+    PCG_STAMP(1);
+    const double pq = grid_allreduce(loc, P, ++epoch, sm);
+    PCG_STAMP(2);
     if (!(pq > 0.0) || !isfinite(pq)) break;
     const double a = rz / pq;
     // phase B: x += a p; r -= a q; z = dinv r; rz_new
     loc = 0.0;
     for (int64_t d = tid; d < nd; d += stride) {
-      const double pv = pnew[d];
+      const double pv = __ldcg(pnew + d);
       P.x[d] = fma(a, pv, P.x[d]);
-      const double rv = fma(-a, P.q[d], P.r[d]);
+      const double rv = fma(-a, __ldcg(P.q + d), P.r[d]);
       P.r[d] = rv;
       const double zv = P.dinv[d] * rv;
       P.z[d] = zv;
       loc = fma(rv, zv, loc);
     }
-    block_partial(loc, &partB[blockIdx.x], sm);
-    grid_barrier(P.bar, ++epoch * nb);
-    const double rzn = grid_total(partB, nb, &tot);
+    PCG_STAMP(3);
+    const double rzn = grid_allreduce(loc, P, ++epoch, sm);
+    PCG_STAMP(4);
     if (!(rzn > 0.0) || !isfinite(rzn)) break;
     beta = rzn / rz;
     rz = rzn;
@@ -224,16 +243,25 @@ void Pcg80::setup(const Grid& g, const double* A, const double* diag, double eps
   for (int32_t d : f2d) fixed[size_t(d)] = 0;
   for (int64_t d = 0; d < nd; ++d) h[size_t(d)] = fixed[size_t(d)] ? 0.0 : 1.0 / (h[size_t(d)] + eps);
   dinv.upload(h.data(), h.size(), s);
-  int dev = 0, nsm = 0, per_sm = 0;
+  int dev = 0, nsm = 0, per_sm = 0, smem_optin = 0;
   SG_CUDA(cudaGetDevice(&dev));
   SG_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-  SG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pcg80_kernel, kPcgThreads, 0));
+  SG_CUDA(cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
   const int64_t want = (g.d.nnodes() + kPcgNodes - 1) / kPcgNodes;
-  // one block per SM at most: the barrier cost grows with the participant count
-  const int64_t cap = int64_t(nsm) * std::min(std::max(per_sm, 1), 1);
-  nblocks = int(std::max<int64_t>(1, std::min(want, cap)));
+  // one block per SM: the barrier cost grows with the participant count, and a
+  // single pass lets every block keep its operator rows in shared memory
+  nblocks = int(std::max<int64_t>(1, std::min<int64_t>(want, nsm)));
+  const int static_smem = 8 * 1024;
+  const int per_slot = 9 * kPcgNodes * int(sizeof(double));
+  cache_slots = 0;
+  if (int64_t(nblocks) * kPcgNodes >= g.d.nnodes())
+    cache_slots = std::max(0, std::min(27, (smem_optin - static_smem) / per_slot));
+  smem_bytes = cache_slots * per_slot;
+  SG_CUDA(cudaFuncSetAttribute(pcg80_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes));
+  SG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pcg80_kernel, kPcgThreads, smem_bytes));
+  SG_REQUIRE(per_sm >= 1, "pcg80 kernel cannot be resident");
   partials.alloc(size_t(2 * nblocks));
-  bar.alloc(1);
+  bar.alloc(size_t(64 * (2 + (nblocks + kBarGroup - 1) / kBarGroup)));
   SG_CUDA(cudaStreamSynchronize(s));
 }
 
@@ -253,10 +281,12 @@ void Pcg80::solve(const double* b, double* x, cudaStream_t s) {
   a.bar = bar.p;
   a.eps = eps;
   a.steps = steps;
-  SG_CUDA(cudaMemsetAsync(bar.p, 0, sizeof(unsigned), s));
+  a.cache_slots = cache_slots;
+  a.trace = trace;
+  SG_CUDA(cudaMemsetAsync(bar.p, 0, sizeof(unsigned) * bar.n, s));
   void* args[] = {&a};
   SG_CUDA(cudaLaunchCooperativeKernel((void*)pcg80_kernel, dim3(nblocks), dim3(kPcgThreads), args,
-                                      0, s));
+                                      size_t(smem_bytes), s));
   SG_CHECK_LAUNCH();
 }
 

@@ -11,11 +11,14 @@ struct Pcg80 {
   double eps = 0.0;
   int steps = 80;
   int nblocks = 0;
+  int cache_slots = 0; // stencil slots resident in shared memory
+  int smem_bytes = 0;
   DBuf<double> dinv, r, z, p0, p1, q, partials;
   DBuf<unsigned> bar;
   void setup(const Grid& g, const double* A, const double* diag, double eps, int steps,
              cudaStream_t s);
   void solve(const double* b, double* x, cudaStream_t s);
+  long long* trace = nullptr;  // development instrumentation (sg_hier_pcg80_trace)
 };
 
 // Dense (K + eps I)^-1 from an on-device Cholesky (hierarchy.py:165-178).
