@@ -246,16 +246,21 @@ def run_gpu(args):
         ms = float(t.item())
         torch.distributed.barrier()
 
-    # end to end through the public API: host b in, host x out
+    # end to end through the public API: b from pinned host memory (H2D inside
+    # the solve call), solution copied back into pinned host memory (D2H)
+    b_pin = torch.from_numpy(b_host).pin_memory()
+    x_pin = torch.empty_like(b_pin).pin_memory()
     e2e = []
     for k in range(max(3, min(args.steps, 5))):
         flush.zero_()
         torch.cuda.synchronize()
         s = time.perf_counter()
-        rep_h = P.pcg(op.matvec, h.vcycle, b_host, cfg)
+        rep_h = P.pcg(op.matvec, h.vcycle, b_pin, cfg)
+        x_pin.copy_(rep_h.x, non_blocking=False)
         torch.cuda.synchronize()
         e2e.append(time.perf_counter() - s)
     e2e_s = sum(e2e) / len(e2e)
+    assert np.allclose(x_pin.numpy(), rep.x.cpu().numpy())
 
     # per-component device timings (CUDA events inside the library)
     def prof(what, reps=10):

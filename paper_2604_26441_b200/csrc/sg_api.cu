@@ -233,7 +233,7 @@ int sg_hier_cycle(sg_hier* h, int gamma, const double* r, double* z, void* strea
     cudaStream_t s = S(stream);
     sg::Level& L0 = *h->h->lv[0];
     sg::scatter_free<double>(*L0.g, r, L0.w.r.p, s);
-    sg::cycle(*h->h, 0, gamma, s);
+    sg::cycle_run(*h->h, gamma, s);
     sg::gather_free<double>(*L0.g, L0.w.x.p, z, s);
   });
 }
@@ -346,7 +346,9 @@ static int run_solver(int which, sg_fine* f, int ktag, sg_hier* h, int gamma, co
     sg::SolveOut o;
     std::vector<double> hist;
     const int64_t nd = 3 * f->op.grid.d.nnodes();
-    sg::DBuf<double> bn(static_cast<size_t>(nd)), xn(static_cast<size_t>(nd));
+    struct {
+      double* p;
+    } bn{f->w.sw.vec(6, nd)}, xn{f->w.sw.vec(7, nd)};
     sg::scatter_free<double>(f->op.grid, b, bn.p, s);
     if (which == 0) sg::pcg_native(sys, bn.p, xn.p, c, o, hist, s);
     else sg::fgmres_native(sys, bn.p, xn.p, c, o, hist, s);
@@ -623,7 +625,7 @@ extern "C" int sg_hier_profile(sg_hier* h, int what, int reps, double* ms_avg, v
           sg::coarsest_solve(H, Lc.w.r.p, Lc.w.x.p, s);
           break;
         }
-        case 4: sg::cycle(H, 0, 1, s); break;
+        case 4: sg::cycle_run(H, 1, s); break;
         case 5: sg::fine_apply_bf16(*H.fine, fa.p, fb.p, s); break;
         default: throw sg::Error("unknown profile target");
       }

@@ -8,6 +8,7 @@
 // FP64.  Elementwise updates use explicit round-to-nearest intrinsics so no
 // FMA contraction changes the numpy-equivalent bits.
 #include <cmath>
+#include <cstdlib>
 #include "sg_hier.cuh"
 
 namespace sg {
@@ -234,6 +235,48 @@ void cycle(Hier& H, int l, int gamma, cudaStream_t s) {
     prolong(*L.g, *C.g, C.w.x.p, x64, /*add=*/true, s);
   }
   level_smooth(H, l, L.w.r.p, x64, L.w.x.p, s);
+}
+
+Hier::~Hier() {
+  for (auto& g : graph)
+    if (g) cudaGraphExecDestroy(g);
+}
+
+void cycle_run(Hier& H, int gamma, cudaStream_t s) {
+  static const bool no_graph = [] {
+    const char* e = std::getenv("SG_NO_GRAPH");
+    return e && e[0] == '1';
+  }();
+  SG_REQUIRE(gamma == 1 || gamma == 2, "gamma must be 1 (V) or 2 (W)");
+  if (no_graph) {
+    cycle(H, 0, gamma, s);
+    return;
+  }
+  if (!H.graph[gamma]) {
+    // capture on a private non-blocking stream (the caller's may be the
+    // legacy NULL stream, which cannot be captured); capture only records
+    cudaStream_t cs = nullptr;
+    SG_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+    cudaGraph_t g = nullptr;
+    SG_CUDA(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+    try {
+      cycle(H, 0, gamma, cs);
+    } catch (...) {
+      cudaStreamEndCapture(cs, &g);
+      if (g) cudaGraphDestroy(g);
+      cudaStreamDestroy(cs);
+      throw;
+    }
+    SG_CUDA(cudaStreamEndCapture(cs, &g));
+    cudaStreamDestroy(cs);
+    size_t n = 0;
+    SG_CUDA(cudaGraphGetNodes(g, nullptr, &n));
+    SG_CUDA(cudaGraphInstantiate(&H.graph[gamma], g, 0));
+    SG_CUDA(cudaGraphDestroy(g));
+    H.graph_nodes[gamma] = n;
+  }
+  SG_CUDA(cudaGraphLaunch(H.graph[gamma], s));
+  __atomic_add_fetch(&g_sg_launches, (unsigned long long)H.graph_nodes[gamma], __ATOMIC_RELAXED);
 }
 
 // ------------------------------------------------------- diag / power

@@ -53,10 +53,38 @@ struct Hier {
   RedWork red;
   DBuf<double> scal;  // device scalars
   DBuf<double> io_a, io_b;  // free<->node staging for the API (fine level)
+  // CUDA graphs of the whole cycle (lv[0]->w.r -> lv[0]->w.x), per gamma
+  cudaGraphExec_t graph[3] = {nullptr, nullptr, nullptr};
+  size_t graph_nodes[3] = {0, 0, 0};
+  ~Hier();
+};
+// One V/W-cycle from lv[0]->w.r into lv[0]->w.x, replayed from a CUDA graph
+// captured on first use (set SG_NO_GRAPH=1 to launch kernel by kernel).
+void cycle_run(Hier& H, int gamma, cudaStream_t s);
+
+// Device scratch of the native solvers, allocated on first use and reused by
+// every later solve (no cudaMalloc/cudaFree -- and their implicit device
+// synchronisation -- inside a solve).
+struct SolverWork {
+  RedWork red;
+  DBuf<double> sc;
+  DBuf<float> t32a, t32b;
+  DBuf<double> v[8];
+  DBuf<double> basis1, basis2;
+  DBuf<double> small;
+  double* vec(int i, int64_t nd) {
+    if (v[i].n < size_t(nd)) v[i].alloc(size_t(nd));
+    return v[i].p;
+  }
+  static double* grow(DBuf<double>& b, size_t n) {
+    if (b.n < n) b.alloc(n);
+    return b.p;
+  }
 };
 
 // Workspace attached to a fine operator for API-level applies.
 struct FineWork {
+  SolverWork sw;
   DBuf<double> u64, y64;
   DBuf<float> u32, y32;
   DBuf<double> diag;  // floored, node layout

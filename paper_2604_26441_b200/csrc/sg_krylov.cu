@@ -114,23 +114,31 @@ __global__ void f32_to_f64_k(int64_t n, const float* __restrict__ a, double* __r
 
 inline int nb256(int64_t n) { return grid_blocks(n, 256); }
 
+struct View {  // non-owning handle on a reused SolverWork buffer
+  double* p;
+};
+
 struct Ctx {
   NativeSys& sys;
   cudaStream_t s;
   int64_t nd;
-  RedWork red;
-  DBuf<double> sc;
-  DBuf<float> t32a, t32b;
-  Ctx(NativeSys& sy, cudaStream_t st) : sys(sy), s(st) {
+  RedWork& red;
+  DBuf<double>& sc;
+  DBuf<float>& t32a;
+  DBuf<float>& t32b;
+  Ctx(NativeSys& sy, cudaStream_t st)
+      : sys(sy), s(st), red(sy.fw->sw.red), sc(sy.fw->sw.sc), t32a(sy.fw->sw.t32a),
+        t32b(sy.fw->sw.t32b) {
     nd = 3 * sys.fine->grid.d.nnodes();
     red.init(s);
-    sc.alloc(256);
+    if (!sc.p) sc.alloc(256);
     SG_CUDA(cudaMemsetAsync(sc.p, 0, 256 * sizeof(double), s));
-    if (sys.ktag != TAG_FP64) {
+    if (sys.ktag != TAG_FP64 && t32a.n < size_t(nd)) {
       t32a.alloc(size_t(nd));
       t32b.alloc(size_t(nd));
     }
   }
+  double* vec(int i) { return sys.fw->sw.vec(i, nd); }
   // y = apply_K(x) promoted to f64 (krylov.py:136: np.asarray(apply_K(p), float64))
   void K(const double* x, double* y) {
     if (sys.ktag == TAG_FP64) {
@@ -147,7 +155,7 @@ struct Ctx {
     if (sys.hier) {
       Level& L0 = *sys.hier->lv[0];
       if (r != L0.w.r.p) copy_k<<<nb256(nd), 256, 0, s>>>(nd, r, L0.w.r.p);
-      cycle(*sys.hier, 0, sys.gamma, s);
+      cycle_run(*sys.hier, sys.gamma, s);
       copy_k<<<nb256(nd), 256, 0, s>>>(nd, L0.w.x.p, z);
     } else {
       mul_k<<<nb256(nd), 256, 0, s>>>(nd, sys.fw->diag_inv_ptr(), r, z);
@@ -204,8 +212,8 @@ void pcg_native(NativeSys& sys, const double* b, double* x, const SolverCfg& cfg
     out = SolveOut{1, 0, 0.0, 0, now() - t0};
     return;
   }
-  DBuf<double> r_own, z(static_cast<size_t>(nd)), p(static_cast<size_t>(nd)), q(static_cast<size_t>(nd));
-  double* r = sys.hier ? sys.hier->lv[0]->w.r.p : (r_own.alloc(size_t(nd)), r_own.p);
+  const View z{C.vec(0)}, p{C.vec(1)}, q{C.vec(2)};
+  double* r = sys.hier ? sys.hier->lv[0]->w.r.p : C.vec(3);
   copy_k<<<nb256(nd), 256, 0, s>>>(nd, b, r);
   C.M(r, z.p);
   copy_k<<<nb256(nd), 256, 0, s>>>(nd, z.p, p.p);
@@ -317,8 +325,10 @@ void fgmres_native(NativeSys& sys, const double* b, double* x, const SolverCfg& 
   }
   const int m = cfg.restart;
   SG_REQUIRE(m + 1 <= 200, "restart too large for the scalar slots");
-  DBuf<double> V(size_t(m + 1) * nd), Z(size_t(m) * nd), w(static_cast<size_t>(nd)),
-      r(static_cast<size_t>(nd)), tmp(static_cast<size_t>(nd)), yv(static_cast<size_t>(m));
+  SolverWork& sw = sys.fw->sw;
+  const View V{SolverWork::grow(sw.basis1, size_t(m + 1) * nd)},
+      Z{SolverWork::grow(sw.basis2, size_t(m) * nd)}, w{C.vec(0)}, r{C.vec(1)}, tmp{C.vec(2)},
+      yv{SolverWork::grow(sw.small, size_t(m))};
   int kind = 1;
   bool done = false;
   while (!done && int(hist.size()) < cfg.maxiter) {
@@ -412,7 +422,7 @@ void fgmres_native(NativeSys& sys, const double* b, double* x, const SolverCfg& 
       for (int i = 0; i < used; ++i)
         for (int k = 0; k < used; ++k) Hs[size_t(i) * used + k] = H[size_t(i) * m + k];
       solve_upper(Hs, used, used, g, y);
-      yv.upload(y.data(), size_t(used), s);
+      SG_CUDA(cudaMemcpyAsync(yv.p, y.data(), sizeof(double) * used, cudaMemcpyHostToDevice, s));
       gemv_t_k<<<nb256(nd), 256, 0, s>>>(nd, used, Z.p, nd, yv.p, x, 1.0);
       SG_CHECK_LAUNCH();
     }
@@ -445,7 +455,7 @@ void lanczos_native(NativeSys& sys, int m, uint64_t seed, std::vector<double>& H
   Ctx C(sys, s);
   const int64_t nd = C.nd;
   SG_REQUIRE(m >= 2 && m <= 200, "Lanczos steps out of range");
-  DBuf<double> Q(size_t(m) * nd), w(static_cast<size_t>(nd)), kv(static_cast<size_t>(nd));
+  const View Q{SolverWork::grow(sys.fw->sw.basis1, size_t(m) * nd)}, w{C.vec(0)}, kv{C.vec(1)};
   H.assign(size_t(m) * m, 0.0);
   used = m;
   partial = false;
