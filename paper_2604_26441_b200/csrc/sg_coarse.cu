@@ -291,68 +291,6 @@ void Pcg80::solve(const double* b, double* x, cudaStream_t s) {
 }
 
 // ------------------------------------------------------------------ dense
-// Unblocked right-looking Cholesky of an n x n SPD matrix (row-major, lower
-// triangle used) by one 1024-thread CTA; returns info > 0 on a non-positive
-// pivot like LAPACK dpotrf.
-__global__ void __launch_bounds__(1024) chol_kernel(int n, double* L, int* info) {
-  __shared__ double piv;
-  __shared__ int bad;
-  if (threadIdx.x == 0) bad = 0;
-  __syncthreads();
-  for (int j = 0; j < n; ++j) {
-    if (threadIdx.x == 0) {
-      const double d = L[int64_t(j) * n + j];
-      if (!(d > 0.0) || !isfinite(d)) {
-        bad = j + 1;
-      } else {
-        piv = sqrt(d);
-        L[int64_t(j) * n + j] = piv;
-      }
-    }
-    __syncthreads();
-    if (bad) break;
-    for (int i = j + 1 + threadIdx.x; i < n; i += blockDim.x) L[int64_t(i) * n + j] /= piv;
-    __syncthreads();
-    // trailing update of the lower triangle: L[i][k] -= L[i][j] * L[k][j], k <= i
-    const int m = n - j - 1;
-    const int64_t tri = int64_t(m) * (m + 1) / 2;
-    for (int64_t t = threadIdx.x; t < tri; t += blockDim.x) {
-      // map t -> (ii, kk) with kk <= ii
-      int ii = int((sqrt(8.0 * double(t) + 1.0) - 1.0) * 0.5);
-      while (int64_t(ii) * (ii + 1) / 2 > t) --ii;
-      while (int64_t(ii + 1) * (ii + 2) / 2 <= t) ++ii;
-      const int kk = int(t - int64_t(ii) * (ii + 1) / 2);
-      const int i = j + 1 + ii, k = j + 1 + kk;
-      L[int64_t(i) * n + k] -= L[int64_t(i) * n + j] * L[int64_t(k) * n + j];
-    }
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) *info = bad;
-}
-
-// Column c of inv(L): forward substitution, one thread per column.
-__global__ void trinv_kernel(int n, const double* __restrict__ L, double* __restrict__ Y) {
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= n) return;
-  for (int i = 0; i < n; ++i) Y[int64_t(i) * n + c] = 0.0;
-  Y[int64_t(c) * n + c] = 1.0 / L[int64_t(c) * n + c];
-  for (int i = c + 1; i < n; ++i) {
-    double s = 0.0;
-    for (int t = c; t < i; ++t) s += L[int64_t(i) * n + t] * Y[int64_t(t) * n + c];
-    Y[int64_t(i) * n + c] = -s / L[int64_t(i) * n + i];
-  }
-}
-
-// Ainv[i][k] = sum_{t >= max(i,k)} Y[t][i] * Y[t][k]
-__global__ void ytY_kernel(int n, const double* __restrict__ Y, double* __restrict__ Ai) {
-  const int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (q >= int64_t(n) * n) return;
-  const int i = int(q / n), k = int(q % n);
-  double s = 0.0;
-  for (int t = i > k ? i : k; t < n; ++t) s += Y[int64_t(t) * n + i] * Y[int64_t(t) * n + k];
-  Ai[q] = s;
-}
-
 __global__ void gemv_node_kernel(int64_t nfree, const int32_t* __restrict__ f2d,
                                  const double* __restrict__ Ai, const double* __restrict__ r,
                                  double* __restrict__ x) {
@@ -371,21 +309,15 @@ bool DenseInverse::setup(const Grid& g, const double* dense_with_eps, cudaStream
   grid = &g;
   n = g.n_free;
   SG_REQUIRE(n > 0 && n <= 20000, "dense coarsest size out of range");
-  DBuf<double> L(static_cast<size_t>(n * n)), Y(static_cast<size_t>(n * n));
+  DBuf<double> L(static_cast<size_t>(n * n));
   SG_CUDA(cudaMemcpyAsync(L.p, dense_with_eps, sizeof(double) * n * n, cudaMemcpyDeviceToDevice, s));
-  DBuf<int> info(1);
-  chol_kernel<<<1, 1024, 0, s>>>(int(n), L.p, info.p);
-  SG_CHECK_LAUNCH();
-  int h_info = 0;
-  info.download(&h_info, 1, s);
-  SG_CUDA(cudaStreamSynchronize(s));
-  if (h_info) return false;  // LinAlgError -> pcg80 fallback (hierarchy.py:172-178)
-  trinv_kernel<<<grid_blocks(n, 64), 64, 0, s>>>(int(n), L.p, Y.p);
-  SG_CHECK_LAUNCH();
   Ainv.alloc(size_t(n * n));
-  ytY_kernel<<<grid_blocks(n * n, 256), 256, 0, s>>>(int(n), Y.p, Ainv.p);
-  SG_CHECK_LAUNCH();
-  SG_CUDA(cudaStreamSynchronize(s));
+  // blocked device Cholesky + inverse (sg_dense.cu); false = LinAlgError ->
+  // pcg80 fallback (hierarchy.py:172-178)
+  if (!dense_spd_inverse(int(n), L.p, Ainv.p, s)) {
+    Ainv.release();
+    return false;
+  }
   return true;
 }
 

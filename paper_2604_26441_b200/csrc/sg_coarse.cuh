@@ -21,6 +21,10 @@ struct Pcg80 {
   long long* trace = nullptr;  // development instrumentation (sg_hier_pcg80_trace)
 };
 
+// Blocked device Cholesky + explicit inverse of an SPD n x n row-major matrix
+// (sg_dense.cu); returns false on a non-positive pivot.
+bool dense_spd_inverse(int n, double* A, double* Ainv, cudaStream_t s);
+
 // Dense (K + eps I)^-1 from an on-device Cholesky (hierarchy.py:165-178).
 struct DenseInverse {
   const Grid* grid = nullptr;
