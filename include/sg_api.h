@@ -152,6 +152,18 @@ int sg_transfer_csr(sg_transfer* t, int64_t* indptr, int64_t* indices, double* d
 int sg_level1_csr(sg_fine* op, const double* triples, const uint32_t* codes, const double* diffs,
                   int ncodes, int64_t* indptr, int64_t* indices, double* data, int64_t* nnz);
 
+/* triple_product (transfer.py:177-181) on ARBITRARY CSR inputs (host arrays,
+ * int64 indices, stored order honoured): canonical CSR of P^T (K P) with
+ * scipy csr_matmat summation order, bit-identical.  nf = rows of P = size of K,
+ * nc = columns of P.  Fetch with sg_csr_result_get (Cp: nc+1, Cj/Cx: nnz). */
+int sg_ptap_csr(int64_t nf, int64_t nc, const int64_t* Pp, const int64_t* Pj, const double* Px,
+                const int64_t* Kp, const int64_t* Kj, const double* Kx, void** result,
+                int64_t* nnz, void* stream);
+int sg_csr_result_get(void* result, int64_t* Cp, int64_t* Cj, double* Cx);
+void sg_csr_result_free(void* result);
+/* Development instrumentation: pcg80 phase timestamps (ns) of block 0, step 10. */
+int sg_hier_pcg80_trace(sg_hier* h, long long* out, void* stream);
+
 /* ---------------------------------------------------------------------
  * Outer solvers (krylov.py)
  * ------------------------------------------------------------------- */

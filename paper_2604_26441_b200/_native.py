@@ -81,6 +81,11 @@ SIGNATURES = {
     "sg_transfer_csr": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, P(c_i64)]),
     "sg_level1_csr": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_int, c_void_p, c_void_p,
                               c_void_p, P(c_i64)]),
+    "sg_ptap_csr": (c_int, [c_i64, c_i64, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
+                            c_void_p, P(c_void_p), P(c_i64), c_void_p]),
+    "sg_csr_result_get": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p]),
+    "sg_csr_result_free": (None, [c_void_p]),
+    "sg_hier_pcg80_trace": (c_int, [c_void_p, c_void_p, c_void_p]),
     "sg_pcg": (c_int, [c_void_p, c_int, c_void_p, c_int, c_void_p, c_void_p, P(SolverCfg),
                        P(Report), c_void_p, c_void_p]),
     "sg_fgmres": (c_int, [c_void_p, c_int, c_void_p, c_int, c_void_p, c_void_p, P(SolverCfg),

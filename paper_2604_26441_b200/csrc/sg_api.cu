@@ -660,3 +660,29 @@ extern "C" int sg_hier_pcg80_trace(sg_hier* h, long long* out, void* stream) {
     SG_CUDA(cudaStreamSynchronize(s));
   });
 }
+
+namespace sg {
+void* ptap_compute(int64_t nf, int64_t nc, const int64_t* Pp, const int64_t* Pj, const double* Px,
+                   const int64_t* Kp, const int64_t* Kj, const double* Kx, int64_t* nnz,
+                   cudaStream_t s);
+void ptap_fetch(void* h, int64_t* Cp, int64_t* Cj, double* Cx);
+void ptap_free(void* h);
+}  // namespace sg
+
+extern "C" {
+
+int sg_ptap_csr(int64_t nf, int64_t nc, const int64_t* Pp, const int64_t* Pj, const double* Px,
+                const int64_t* Kp, const int64_t* Kj, const double* Kx, void** result,
+                int64_t* nnz, void* stream) {
+  return guard([&] {
+    *result = sg::ptap_compute(nf, nc, Pp, Pj, Px, Kp, Kj, Kx, nnz, S(stream));
+  });
+}
+
+int sg_csr_result_get(void* result, int64_t* Cp, int64_t* Cj, double* Cx) {
+  return guard([&] { sg::ptap_fetch(result, Cp, Cj, Cx); });
+}
+
+void sg_csr_result_free(void* result) { sg::ptap_free(result); }
+
+}  // extern "C"
