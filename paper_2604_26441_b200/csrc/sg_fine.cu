@@ -6,6 +6,7 @@
 // contributions of its <= 8 adjacent elements in ascending element order, so
 // no atomics are needed and every result is bit-reproducible run to run.
 // The modulus is applied after the element contraction, as in the reference.
+#include <cstdlib>
 #include "sg_kernels.cuh"
 
 namespace sg {
@@ -115,8 +116,18 @@ void fine_apply_f32(const FineOp& op, const float* u, float* y, cudaStream_t s) 
   if (op.walsh_ok) fine_apply_walsh_f32(op, u, y, s);
   else fine_apply_dense_f32(op, u, y, s);
 }
-void fine_apply_bf16(const FineOp& op, const float* u, float* y, cudaStream_t s) {
+void fine_apply_bf16_dense(const FineOp& op, const float* u, float* y, cudaStream_t s) {
   launch_apply<float, 2>(op.grid.d, op.grid.nmask.p, u, y, op.E32.p, op.ke16, s);
+}
+// BF16EMU runs on the tensor cores (tcgen05, sg_fine_tc.cu); SG_BF16_DENSE=1
+// selects the CUDA-core reference kernel (used by the parity tests).
+void fine_apply_bf16(const FineOp& op, const float* u, float* y, cudaStream_t s) {
+  static const bool dense = [] {
+    const char* e = std::getenv("SG_BF16_DENSE");
+    return e && e[0] == '1';
+  }();
+  if (dense) fine_apply_bf16_dense(op, u, y, s);
+  else fine_apply_bf16_tc(op, u, y, s);
 }
 
 void fine_diag_raw(const FineOp& op, double* d, cudaStream_t s) {

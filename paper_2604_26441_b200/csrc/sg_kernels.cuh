@@ -46,6 +46,8 @@ void fine_apply_dense_f32(const FineOp& op, const float* u, float* y, cudaStream
 void fine_apply_dense_f64(const FineOp& op, const double* u, double* y, cudaStream_t s);
 void fine_apply_f32(const FineOp& op, const float* u, float* y, cudaStream_t s);
 void fine_apply_bf16(const FineOp& op, const float* u, float* y, cudaStream_t s);
+void fine_apply_bf16_tc(const FineOp& op, const float* u, float* y, cudaStream_t s);
+void fine_apply_bf16_dense(const FineOp& op, const float* u, float* y, cudaStream_t s);
 void fine_diag_raw(const FineOp& op, double* d, cudaStream_t s);
 
 // ------------------------------------------------------ grids and vectors
