@@ -276,12 +276,14 @@ def run_gpu(args):
     tl1 = prof(2)
     tco = prof(3)
     tvc = prof(4)
+    tbf = prof(5)
     peak, peak_kind = _peaks()
     b32 = 8 * n_free + 4 * n_elem
     b64 = 16 * n_free + 8 * n_elem
     bl1 = (243 * 8 + 48) * nn1
     comps["fine_apply_fp32"] = {"ms": t32, "alg_bytes": b32, "gbs": b32 / t32 / 1e6}
     comps["fine_apply_fp64"] = {"ms": t64, "alg_bytes": b64, "gbs": b64 / t64 / 1e6}
+    comps["fine_apply_bf16_tcgen05"] = {"ms": tbf, "alg_bytes": b32, "gbs": b32 / tbf / 1e6}
     comps["level1_spmv_fp64"] = {"ms": tl1, "alg_bytes": bl1, "gbs": bl1 / tl1 / 1e6}
     comps["coarsest_pcg80"] = {"ms": tco}
     comps["vcycle"] = {"ms": tvc}
@@ -302,7 +304,7 @@ def run_gpu(args):
         "pcg_iters": iters[-1], "final_true_residual": rep.final_true_residual,
         "converged": bool(rep.converged), "setup_s": setup_s,
         "fine_matvec_gbs": achieved,
-        "roofline": {"kernel": "fine_apply_fp32 (fine_apply_kernel<float,1>)", "bound": "hbm",
+        "roofline": {"kernel": "fine_apply_fp32 (fine_apply_walsh_kernel<float>)", "bound": "hbm",
                      "achieved": achieved, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
                      "alg_bytes_per_launch": b32, "launch_ms": t32},

@@ -193,6 +193,41 @@ int sg_lanczos(sg_fine* op, sg_hier* h, int gamma, int m, uint64_t seed, double*
                int* partial, void* stream);
 
 /* ---------------------------------------------------------------------
+ * Multi-GPU slab partition (BASELINE.json north_star: fine and first coarse
+ * levels slab-partitioned over the GPUs of one node, halo exchange and PCG dot
+ * allreduce over NCCL, deeper levels gathered).  The
+ * reference is single-process, so these extend pcg(op.matvec, h.vcycle, b,
+ * cfg) (krylov.py:113-165, bench/runner.py:66-88) with per-rank z-slab
+ * windows: every rank passes the same global b and receives the same global x.
+ * Data movement between ranks is delegated to the host's sg_comm callbacks
+ * (torch.distributed over NCCL in paper_2604_26441_b200/slab.py); each is
+ * stream-ordered on `stream` and returns 0 on success.
+ * ------------------------------------------------------------------- */
+typedef struct {
+  void* ctx;
+  /* fill the ghost node planes of a window vector of slab level `level` */
+  int (*halo)(void* ctx, int level, void* vec, int elem_bytes, void* stream);
+  /* in-place sum over ranks of n device doubles, in rank order */
+  int (*allreduce)(void* ctx, double* vals, int n, void* stream);
+  /* owned planes of every rank's window vector `win` -> full-grid vector `full` */
+  int (*allgather)(void* ctx, int level, const double* win, double* full, void* stream);
+} sg_comm;
+typedef struct sg_dist sg_dist;
+/* planes: n_dist x {w0, w1, o0, o1} global node planes of this rank's window
+ * [w0, w1] and owned range [o0, o1) on slab levels 0..n_dist-1 (n_dist 1 or 2). */
+int sg_dist_create(sg_hier* h, int n_dist, const int32_t* planes, const sg_comm* comm,
+                   void* stream, sg_dist** out);
+void sg_dist_destroy(sg_dist* d);
+/* method 0 = pcg (krylov.py:113-165), 1 = fgmres (krylov.py:168-281), with
+ * apply_K = op.matvec under ktag and apply_M = V (gamma 1) / W (gamma 2) cycle. */
+int sg_dist_solve(sg_dist* d, int method, int ktag, int gamma, const double* b_free,
+                  double* x_free, const sg_solver_cfg* cfg, sg_report* rep, double* history,
+                  void* stream);
+/* what 0: y = K_ktag x (fine_operator.py:56-77); what 1: y = cycle(x) (hierarchy.py:207-216) */
+int sg_dist_apply(sg_dist* d, int what, int ktag, int gamma, const double* x_free, double* y_free,
+                  void* stream);
+
+/* ---------------------------------------------------------------------
  * Deterministic device vector kernels for the generic (callable) Krylov and
  * smoother paths.  dtype: 0 = double, 1 = float.  All FMA-free.
  * ------------------------------------------------------------------- */

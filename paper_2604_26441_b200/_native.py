@@ -44,6 +44,17 @@ class Report(C.Structure):
                 ("wall_time", c_double)]
 
 
+HALO_FN = C.CFUNCTYPE(c_int, c_void_p, c_int, c_void_p, c_int, c_void_p)
+ALLREDUCE_FN = C.CFUNCTYPE(c_int, c_void_p, c_void_p, c_int, c_void_p)
+ALLGATHER_FN = C.CFUNCTYPE(c_int, c_void_p, c_int, c_void_p, c_void_p, c_void_p)
+
+
+class Comm(C.Structure):
+    """sg_comm: host callbacks of the slab partition (include/sg_api.h)."""
+    _fields_ = [("ctx", c_void_p), ("halo", HALO_FN), ("allreduce", ALLREDUCE_FN),
+                ("allgather", ALLGATHER_FN)]
+
+
 # name: (restype, argtypes) -- mirrors include/sg_api.h
 SIGNATURES = {
     "sg_last_error": (C.c_char_p, []),
@@ -92,6 +103,11 @@ SIGNATURES = {
                           P(Report), c_void_p, c_void_p]),
     "sg_lanczos": (c_int, [c_void_p, c_void_p, c_int, c_int, c_u64, c_void_p, P(c_int),
                            P(c_int), c_void_p]),
+    "sg_dist_create": (c_int, [c_void_p, c_int, c_void_p, P(Comm), c_void_p, P(c_void_p)]),
+    "sg_dist_destroy": (None, [c_void_p]),
+    "sg_dist_solve": (c_int, [c_void_p, c_int, c_int, c_int, c_void_p, c_void_p, P(SolverCfg),
+                              P(Report), c_void_p, c_void_p]),
+    "sg_dist_apply": (c_int, [c_void_p, c_int, c_int, c_int, c_void_p, c_void_p, c_void_p]),
     "sg_vec_dot": (c_int, [c_int, c_i64, c_void_p, c_void_p, P(c_double), c_void_p]),
     "sg_vec_axpy": (c_int, [c_int, c_i64, c_double, c_void_p, c_void_p, c_void_p]),
     "sg_vec_xpby": (c_int, [c_int, c_i64, c_void_p, c_double, c_void_p, c_void_p]),

@@ -18,6 +18,11 @@ struct sg_hier {
   std::mutex mu;
 };
 
+struct sg_dist {
+  sg_hier* hier = nullptr;
+  std::unique_ptr<sg::DistPart> d;
+};
+
 namespace {
 
 thread_local std::string g_err;
@@ -371,6 +376,91 @@ int sg_pcg(sg_fine* f, int ktag, sg_hier* h, int gamma, const double* b, double*
 int sg_fgmres(sg_fine* f, int ktag, sg_hier* h, int gamma, const double* b, double* x,
               const sg_solver_cfg* cfg, sg_report* rep, double* history, void* stream) {
   return run_solver(1, f, ktag, h, gamma, b, x, cfg, rep, history, stream);
+}
+
+// ------------------------------------------------------- slab partition
+int sg_dist_create(sg_hier* h, int n_dist, const int32_t* planes, const sg_comm* comm, void* stream,
+                   sg_dist** out) {
+  return guard([&] {
+    SG_REQUIRE(h && planes && comm && out && comm->halo && comm->allreduce && comm->allgather,
+               "null argument");
+    std::lock_guard<std::mutex> lk(h->mu);
+    sg::CommHooks c;
+    c.ctx = comm->ctx;
+    c.halo = comm->halo;
+    c.allreduce = comm->allreduce;
+    c.allgather = comm->allgather;
+    std::vector<int> pl(planes, planes + 4 * n_dist);
+    auto d = std::make_unique<sg_dist>();
+    d->hier = h;
+    d->d = sg::dist_build(*h->h, n_dist, pl.data(), c, S(stream));
+    *out = d.release();
+  });
+}
+
+void sg_dist_destroy(sg_dist* d) { delete d; }
+
+namespace {
+// global free vector -> this rank's window (node layout)
+void to_window(sg::DistPart& D, const double* x_free, double* xw, cudaStream_t s) {
+  const sg::Grid& fg = D.full->fine->grid;
+  sg::scatter_free<double>(fg, x_free, D.bfull.p, s);
+  SG_CUDA(cudaMemcpyAsync(xw, D.bfull.p + int64_t(D.w0[0]) * D.plane_nd(0),
+                          sizeof(double) * D.W->lv[0]->nd(), cudaMemcpyDeviceToDevice, s));
+}
+// owned planes of every rank -> global free vector
+void from_window(sg::DistPart& D, const double* yw, double* y_free, cudaStream_t s) {
+  D.comm.gather(0, yw, D.xfull.p, s);
+  sg::gather_free<double>(D.full->fine->grid, D.xfull.p, y_free, s);
+}
+}  // namespace
+
+int sg_dist_solve(sg_dist* dd, int method, int ktag, int gamma, const double* b, double* x,
+                  const sg_solver_cfg* cfg, sg_report* rep, double* history, void* stream) {
+  return guard([&] {
+    SG_REQUIRE(dd && cfg && rep, "null argument");
+    std::unique_lock<std::mutex> lf(dd->hier->fine->mu);
+    std::unique_lock<std::mutex> lh(dd->hier->mu);
+    sg::DistPart& D = *dd->d;
+    cudaStream_t s = S(stream);
+    sg::NativeSys sys{&D.wfine, &D.wfw, ktag, D.W.get(), gamma, &D};
+    sg::SolverCfg c{cfg->tol, cfg->maxiter, cfg->restart};
+    sg::SolveOut o;
+    std::vector<double> hist;
+    const int64_t nd = D.W->lv[0]->nd();
+    double* bw = D.wfw.sw.vec(6, nd);
+    double* xw = D.wfw.sw.vec(7, nd);
+    to_window(D, b, bw, s);
+    if (method == 0) sg::pcg_native(sys, bw, xw, c, o, hist, s);
+    else sg::fgmres_native(sys, bw, xw, c, o, hist, s);
+    from_window(D, xw, x, s);
+    SG_CUDA(cudaStreamSynchronize(s));
+    rep->converged = o.converged;
+    rep->iterations = o.iterations;
+    rep->final_true_residual = o.final_true_residual;
+    rep->failure_kind = o.failure_kind;
+    rep->wall_time = o.wall_time;
+    if (history) std::copy(hist.begin(), hist.end(), history);
+  });
+}
+
+int sg_dist_apply(sg_dist* dd, int what, int ktag, int gamma, const double* x, double* y,
+                  void* stream) {
+  return guard([&] {
+    SG_REQUIRE(dd && x && y, "null argument");
+    std::unique_lock<std::mutex> lf(dd->hier->fine->mu);
+    std::unique_lock<std::mutex> lh(dd->hier->mu);
+    sg::DistPart& D = *dd->d;
+    cudaStream_t s = S(stream);
+    sg::NativeSys sys{&D.wfine, &D.wfw, ktag, D.W.get(), gamma, &D};
+    const int64_t nd = D.W->lv[0]->nd();
+    double* xw = D.wfw.sw.vec(4, nd);
+    double* yw = D.wfw.sw.vec(5, nd);
+    to_window(D, x, xw, s);
+    sg::dist_apply(sys, what, xw, yw, s);
+    from_window(D, yw, y, s);
+    SG_CUDA(cudaStreamSynchronize(s));
+  });
 }
 
 int sg_lanczos(sg_fine* f, sg_hier* h, int gamma, int m, uint64_t seed, double* H, int* used,

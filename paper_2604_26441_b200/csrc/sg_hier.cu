@@ -9,6 +9,7 @@
 // FMA contraction changes the numpy-equivalent bits.
 #include <cmath>
 #include <cstdlib>
+#include <cstring>
 #include "sg_hier.cuh"
 
 namespace sg {
@@ -78,6 +79,10 @@ __global__ void residual_kernel(int64_t n, const double* __restrict__ r, const T
   SG_ELEMWISE(n);
   d[i_] = __dsub_rn(r[i_], double(y[i_]));
 }
+__global__ void add_kernel(int64_t n, const double* __restrict__ a, double* __restrict__ x) {
+  SG_ELEMWISE(n);
+  x[i_] = __dadd_rn(x[i_], a[i_]);
+}
 __global__ void copy_kernel(int64_t n, const double* __restrict__ a, double* __restrict__ b) {
   SG_ELEMWISE(n);
   b[i_] = a[i_];
@@ -107,6 +112,7 @@ void fine_apply_tag(const FineOp& op, int tag, const void* x, void* y, cudaStrea
 }
 
 void level_apply(Hier& H, Level& L, int tag, const void* x, void* y, cudaStream_t s) {
+  if (H.comm) H.comm->exchange(L.idx, x, tag == TAG_FP64 ? 8 : 4, s);
   if (L.is_fine) {
     fine_apply_tag(*H.fine, tag, x, y, s);
     return;
@@ -463,6 +469,161 @@ std::unique_ptr<Hier> hier_build(FineOp* fine, FineWork& fw, const HParams& p, c
   H->io_b.alloc(nd0);
   SG_CUDA(cudaStreamSynchronize(s));
   return H;
+}
+
+// ------------------------------------------------------ multi-GPU slabs
+// Same recursion and rounding points as cycle(); every operator input is
+// halo-exchanged first (level_apply through W.comm, explicitly before the
+// transfers), so owned rows see exactly the single-GPU operands.  At the
+// cut level the residual is allgathered into the replicated full hierarchy,
+// the coarse tail runs there, and the prolonged correction (P x_c formed
+// first, then added: the bits of prolong(add=true)) is sliced back.
+static void dist_level(DistPart& D, int l, int gamma, cudaStream_t s) {
+  Hier& W = *D.W;
+  Hier& F = *D.full;
+  Level& L = *W.lv[size_t(l)];
+  const int64_t n = L.nd();
+  double* x64 = L.w.d64.p;
+  level_smooth(W, l, L.w.r.p, nullptr, x64, s);
+  for (int g = 0; g < gamma; ++g) {
+    if (L.tag == TAG_FP64) {
+      level_apply(W, L, TAG_FP64, x64, L.w.y64.p, s);
+      launch_ew(n, s, [&](int nb, int nt) { residual_kernel<double><<<nb, nt, 0, s>>>(n, L.w.r.p, L.w.y64.p, L.w.x.p); });
+    } else {
+      cvt_f64_to_f32(n, x64, L.w.x32.p, s);
+      level_apply(W, L, L.tag, L.w.x32.p, L.w.y32.p, s);
+      launch_ew(n, s, [&](int nb, int nt) { residual_kernel<float><<<nb, nt, 0, s>>>(n, L.w.r.p, L.w.y32.p, L.w.x.p); });
+    }
+    if (l + 1 < D.n_dist) {
+      Level& C = *W.lv[size_t(l + 1)];
+      D.comm.exchange(l, L.w.x.p, 8, s);
+      restrict_(*L.g, *C.g, L.w.x.p, C.w.r.p, s);
+      dist_level(D, l + 1, gamma, s);
+      D.comm.exchange(l + 1, C.w.x.p, 8, s);
+      prolong(*L.g, *C.g, C.w.x.p, x64, /*add=*/true, s);
+    } else {
+      Level& FL = *F.lv[size_t(l)];
+      Level& FC = *F.lv[size_t(l + 1)];
+      D.comm.gather(l, L.w.x.p, FL.w.x.p, s);
+      restrict_(*FL.g, *FC.g, FL.w.x.p, FC.w.r.p, s);
+      cycle(F, l + 1, gamma, s);
+      prolong(*FL.g, *FC.g, FC.w.x.p, FL.w.y64.p, /*add=*/false, s);
+      const double* slice = FL.w.y64.p + int64_t(D.w0[l]) * D.plane_nd(l);
+      launch_ew(n, s, [&](int nb, int nt) { add_kernel<<<nb, nt, 0, s>>>(n, slice, x64); });
+    }
+  }
+  level_smooth(W, l, L.w.r.p, x64, L.w.x.p, s);
+}
+
+void dist_cycle(DistPart& D, int gamma, cudaStream_t s) {
+  SG_REQUIRE(gamma == 1 || gamma == 2, "gamma must be 1 (V) or 2 (W)");
+  dist_level(D, 0, gamma, s);
+}
+
+template <class T>
+static void copy_planes(const T* src, int64_t src_nn, T* dst, int64_t dst_nn, int64_t node_off,
+                        int rows, cudaStream_t s) {
+  // dst[q*dst_nn + m] = src[q*src_nn + node_off + m], q < rows (SoA stencil slabs)
+  SG_CUDA(cudaMemcpy2DAsync(dst, sizeof(T) * dst_nn, src + node_off, sizeof(T) * src_nn,
+                            sizeof(T) * dst_nn, rows, cudaMemcpyDeviceToDevice, s));
+}
+
+std::unique_ptr<DistPart> dist_build(Hier& F, int n_dist, const int* planes, const CommHooks& c,
+                                     cudaStream_t s) {
+  SG_REQUIRE(n_dist >= 1 && n_dist <= 2, "1 or 2 slab-partitioned levels");
+  SG_REQUIRE(int(F.lv.size()) > n_dist, "the hierarchy needs a level below the slab levels");
+  auto D = std::make_unique<DistPart>();
+  D->n_dist = n_dist;
+  D->comm = c;
+  D->full = &F;
+  for (int l = 0; l < n_dist; ++l) {
+    D->w0[l] = planes[4 * l + 0];
+    D->w1[l] = planes[4 * l + 1];
+    D->o0[l] = planes[4 * l + 2];
+    D->o1[l] = planes[4 * l + 3];
+    SG_REQUIRE(D->w0[l] <= D->o0[l] && D->o0[l] < D->o1[l] && D->o1[l] <= D->w1[l] + 1 &&
+                   D->w1[l] <= F.lv[size_t(l)]->g->d.nz,
+               "inconsistent slab plan");
+  }
+  if (n_dist == 2)
+    SG_REQUIRE(D->w0[0] == 2 * D->w0[1] && D->w1[0] == std::min(2 * D->w1[1], F.lv[0]->g->d.nz),
+               "level-0 window must be the fine image of the level-1 window");
+  // level-0 window operator: same element matrix, the window's element layers of E
+  const FineOp& ff = *F.fine;
+  FineOp& wf = D->wfine;
+  build_window_grid(ff.grid, D->w0[0], D->w1[0], wf.grid, s);
+  const int64_t layer = int64_t(ff.grid.d.nx) * ff.grid.d.ny;
+  const int64_t ne = wf.grid.d.nelem();
+  wf.E64.alloc(size_t(ne));
+  wf.E32.alloc(size_t(ne));
+  SG_CUDA(cudaMemcpyAsync(wf.E64.p, ff.E64.p + D->w0[0] * layer, sizeof(double) * ne, cudaMemcpyDeviceToDevice, s));
+  SG_CUDA(cudaMemcpyAsync(wf.E32.p, ff.E32.p + D->w0[0] * layer, sizeof(float) * ne, cudaMemcpyDeviceToDevice, s));
+  std::memcpy(wf.ke_host, ff.ke_host, sizeof(wf.ke_host));
+  wf.ke64 = ff.ke64;
+  wf.ke32 = ff.ke32;
+  wf.ke16 = ff.ke16;
+  wf.kdiag = ff.kdiag;
+  wf.kw64 = ff.kw64;
+  wf.kw32 = ff.kw32;
+  wf.walsh_ok = ff.walsh_ok;
+  wf.emax = ff.emax;
+
+  auto W = std::make_unique<Hier>();
+  W->fine = &wf;
+  W->policy = F.policy;
+  W->emax = F.emax;
+  W->comm = &D->comm;
+  W->scal.alloc(16);
+  W->red.init(s);
+  for (int l = 0; l < n_dist; ++l) {
+    const Level& FL = *F.lv[size_t(l)];
+    auto L = std::make_unique<Level>();
+    L->idx = l;
+    L->tag = FL.tag;
+    L->kind = FL.kind;
+    L->degree = FL.degree;
+    L->alpha = FL.alpha;
+    L->omega = FL.omega;
+    L->lam = FL.lam;
+    if (l == 0) {
+      L->is_fine = true;
+      L->g = &wf.grid;
+    } else {
+      build_window_grid(*FL.g, D->w0[l], D->w1[l], L->own, s);
+      L->g = &L->own;
+      const int64_t nnf = FL.g->d.nnodes(), nnw = L->own.d.nnodes();
+      const int64_t off = int64_t(D->w0[l]) * (FL.g->d.nx + 1) * (FL.g->d.ny + 1);
+      L->st.A64.alloc(size_t(243 * nnw));
+      copy_planes(FL.st.A64.p, nnf, L->st.A64.p, nnw, off, 243, s);
+      if (FL.st.A32.p) {
+        L->st.A32.alloc(size_t(243 * nnw));
+        copy_planes(FL.st.A32.p, nnf, L->st.A32.p, nnw, off, 243, s);
+      }
+    }
+    const int64_t n = 3 * L->g->d.nnodes();
+    const int64_t voff = int64_t(D->w0[l]) * 3 * (FL.g->d.nx + 1) * (FL.g->d.ny + 1);
+    L->diag.alloc(size_t(n));
+    L->dinv.alloc(size_t(n));
+    L->dinv32.alloc(size_t(n));
+    SG_CUDA(cudaMemcpyAsync(L->diag.p, FL.diag.p + voff, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
+    SG_CUDA(cudaMemcpyAsync(L->dinv.p, FL.dinv.p + voff, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
+    SG_CUDA(cudaMemcpyAsync(L->dinv32.p, FL.dinv32.p + voff, sizeof(float) * n, cudaMemcpyDeviceToDevice, s));
+    alloc_work(*L);
+    for (auto* b : {&L->w.r, &L->w.x, &L->w.d64, &L->w.y64, &L->w.dd64}) b->zero(s);
+    for (auto* b : {&L->w.b32, &L->w.x32, &L->w.y32, &L->w.dd32}) b->zero(s);
+    W->lv.push_back(std::move(L));
+  }
+  D->W = std::move(W);
+  // flat-Jacobi scratch of the window operator (1/diag of level 0)
+  D->wfw.dinv.alloc(size_t(D->W->lv[0]->nd()));
+  SG_CUDA(cudaMemcpyAsync(D->wfw.dinv.p, D->W->lv[0]->dinv.p, sizeof(double) * D->W->lv[0]->nd(),
+                          cudaMemcpyDeviceToDevice, s));
+  D->wfw.diag_ready = true;
+  const size_t ndf = size_t(F.lv[0]->nd());
+  D->bfull.alloc(ndf);
+  D->xfull.alloc(ndf);
+  SG_CUDA(cudaStreamSynchronize(s));
+  return D;
 }
 
 }  // namespace sg

@@ -18,6 +18,28 @@ struct HParams {
   uint64_t power_seed = 0;
 };
 
+// Host callbacks that move slab data between ranks (multi-GPU slab
+// partition; implemented over torch.distributed / NCCL by the host layer).
+// All are stream-ordered on the stream they are given.
+struct CommHooks {
+  void* ctx = nullptr;
+  // fill the ghost node planes of a window vector of distributed level `level`
+  int (*halo)(void* ctx, int level, void* vec, int elem_bytes, void* stream) = nullptr;
+  // in-place sum over ranks of n device doubles, summed in rank order (same bits everywhere)
+  int (*allreduce)(void* ctx, double* vals, int n, void* stream) = nullptr;
+  // owned planes of every rank's window vector -> the full-grid vector, on every rank
+  int (*allgather)(void* ctx, int level, const double* win, double* full, void* stream) = nullptr;
+  void exchange(int level, const void* v, int eb, cudaStream_t s) const {
+    if (halo(ctx, level, const_cast<void*>(v), eb, s)) throw Error("slab halo exchange failed");
+  }
+  void sum(double* v, int n, cudaStream_t s) const {
+    if (allreduce(ctx, v, n, s)) throw Error("slab allreduce failed");
+  }
+  void gather(int level, const double* win, double* full, cudaStream_t s) const {
+    if (allgather(ctx, level, win, full, s)) throw Error("slab allgather failed");
+  }
+};
+
 // Scratch vectors of one level (node layout).
 struct LevelWork {
   DBuf<double> r, x, d64, y64, dd64;
@@ -56,6 +78,7 @@ struct Hier {
   // CUDA graphs of the whole cycle (lv[0]->w.r -> lv[0]->w.x), per gamma
   cudaGraphExec_t graph[3] = {nullptr, nullptr, nullptr};
   size_t graph_nodes[3] = {0, 0, 0};
+  const CommHooks* comm = nullptr;  // slab windows: halo before every level apply
   ~Hier();
 };
 // One V/W-cycle from lv[0]->w.r into lv[0]->w.x, replayed from a CUDA graph
@@ -121,18 +144,44 @@ struct SolveOut {
 };
 
 // Preconditioner / operator bundle for the native Krylov drivers.
+struct DistPart;
 struct NativeSys {
   FineOp* fine;
   FineWork* fw;
   int ktag;      // tag of apply_K (FineOperator.precision)
   Hier* hier;    // nullptr => Jacobi (1/diag)
   int gamma;     // 1 V-cycle, 2 W-cycle
+  DistPart* dist = nullptr;  // slab-partitioned solve (fine = this rank's window)
 };
+
+// ------------------------------------------------------ multi-GPU slabs
+// One rank's part of a slab-partitioned hierarchy: levels 0..n_dist-1 are
+// z-slab windows (owned node planes + ghost planes), the coarser levels are
+// the replicated full hierarchy `full` (visited after an allgather of the
+// cut level's residual).  Plane numbers are global node planes per level.
+struct DistPart {
+  int n_dist = 0;
+  int w0[2] = {0, 0}, w1[2] = {0, 0}, o0[2] = {0, 0}, o1[2] = {0, 0};
+  CommHooks comm;
+  Hier* full = nullptr;
+  FineOp wfine;                  // level-0 window operator
+  FineWork wfw;                  // its solver scratch
+  std::unique_ptr<Hier> W;       // window levels (W->lv[0] fine window, W->lv[1] L1 window)
+  DBuf<double> bfull, xfull;     // full level-0 node vectors (API boundary)
+  int64_t plane_nd(int l) const { return 3 * int64_t(W->lv[size_t(l)]->g->d.nx + 1) * (W->lv[size_t(l)]->g->d.ny + 1); }
+  int64_t own_off(int l) const { return (o0[l] - w0[l]) * plane_nd(l); }
+  int64_t own_n(int l) const { return (o1[l] - o0[l]) * plane_nd(l); }
+};
+std::unique_ptr<DistPart> dist_build(Hier& full, int n_dist, const int* planes, const CommHooks& c,
+                                     cudaStream_t s);
+// one distributed V/W-cycle: W->lv[0]->w.r -> W->lv[0]->w.x
+void dist_cycle(DistPart& D, int gamma, cudaStream_t s);
 
 void pcg_native(NativeSys& sys, const double* b_node, double* x_node, const SolverCfg& cfg,
                 SolveOut& out, std::vector<double>& hist, cudaStream_t s);
 void fgmres_native(NativeSys& sys, const double* b_node, double* x_node, const SolverCfg& cfg,
                    SolveOut& out, std::vector<double>& hist, cudaStream_t s);
+void dist_apply(NativeSys& sys, int what, const double* xw, double* yw, cudaStream_t s);
 // Lanczos on v -> M(K v); returns H (m x m, row-major) and the number of steps used.
 void lanczos_native(NativeSys& sys, int m, uint64_t seed, std::vector<double>& H, int& used,
                     bool& partial, cudaStream_t s);

@@ -54,6 +54,7 @@ void fine_diag_raw(const FineOp& op, double* d, cudaStream_t s);
 void build_grid(Grid& g, int nx, int ny, int nz, const uint8_t* dof_mask_host /*nullable*/,
                 cudaStream_t s);
 void build_coarse_grid(const Grid& fine, Grid& coarse, cudaStream_t s);
+void build_window_grid(const Grid& full, int k0, int k1, Grid& win, cudaStream_t s);
 
 template <class T>
 void gather_free(const Grid& g, const T* node_vec, T* free_vec, cudaStream_t s);

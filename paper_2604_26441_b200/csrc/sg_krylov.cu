@@ -16,7 +16,7 @@ namespace sg {
 
 namespace {
 
-enum Slot { S_NB = 0, S_PQ, S_RZ, S_RR, S_OK, S_RZN, S_TR, S_BETA, S_H0 = 16 };
+enum Slot { S_NB = 0, S_PQ, S_RZ, S_RR, S_OK, S_RZN, S_TR, S_BETA, S_TMP, S_H0 = 16 };
 
 struct Dot {
   const double* a;
@@ -118,10 +118,17 @@ struct View {  // non-owning handle on a reused SolverWork buffer
   double* p;
 };
 
+template <class Post>
+__global__ void post1_kernel(const double* __restrict__ v, Post p) {
+  const double t[1] = {*v};
+  p(t);
+}
+
 struct Ctx {
   NativeSys& sys;
   cudaStream_t s;
   int64_t nd;
+  int64_t off = 0, nown = 0;  // reduction range: this rank's owned planes (all of nd on 1 GPU)
   RedWork& red;
   DBuf<double>& sc;
   DBuf<float>& t32a;
@@ -130,6 +137,11 @@ struct Ctx {
       : sys(sy), s(st), red(sy.fw->sw.red), sc(sy.fw->sw.sc), t32a(sy.fw->sw.t32a),
         t32b(sy.fw->sw.t32b) {
     nd = 3 * sys.fine->grid.d.nnodes();
+    nown = nd;
+    if (sys.dist) {
+      off = sys.dist->own_off(0);
+      nown = sys.dist->own_n(0);
+    }
     red.init(s);
     if (!sc.p) sc.alloc(256);
     SG_CUDA(cudaMemsetAsync(sc.p, 0, 256 * sizeof(double), s));
@@ -141,6 +153,7 @@ struct Ctx {
   double* vec(int i) { return sys.fw->sw.vec(i, nd); }
   // y = apply_K(x) promoted to f64 (krylov.py:136: np.asarray(apply_K(p), float64))
   void K(const double* x, double* y) {
+    if (sys.dist) sys.dist->comm.exchange(0, x, 8, s);
     if (sys.ktag == TAG_FP64) {
       fine_apply_f64(*sys.fine, x, y, s);
     } else {
@@ -155,15 +168,31 @@ struct Ctx {
     if (sys.hier) {
       Level& L0 = *sys.hier->lv[0];
       if (r != L0.w.r.p) copy_k<<<nb256(nd), 256, 0, s>>>(nd, r, L0.w.r.p);
-      cycle_run(*sys.hier, sys.gamma, s);
+      if (sys.dist) dist_cycle(*sys.dist, sys.gamma, s);
+      else cycle_run(*sys.hier, sys.gamma, s);
       copy_k<<<nb256(nd), 256, 0, s>>>(nd, L0.w.x.p, z);
     } else {
       mul_k<<<nb256(nd), 256, 0, s>>>(nd, sys.fw->diag_inv_ptr(), r, z);
     }
     SG_CHECK_LAUNCH();
   }
+  // reduction of f over the owned range into `slot`, then post(total).  On one
+  // GPU this is a single fused launch; on slabs the partial is summed over
+  // ranks (rank order) before post runs.
+  template <class F, class Post>
+  void reduce(const F& f, const Post& post, int slot) {
+    if (!sys.dist) {
+      launch_reduce<1>(nown, f, post, red, s);
+      return;
+    }
+    launch_reduce<1>(nown, f, StoreTo<1>{{sc.p + slot}}, red, s);
+    sys.dist->comm.sum(sc.p + slot, 1, s);
+    post1_kernel<<<1, 1, 0, s>>>(sc.p + slot, post);
+    SG_CHECK_LAUNCH();
+  }
   void dot(const double* a, const double* b, int slot) {
-    launch_reduce<1>(nd, Dot{a, b}, StoreTo<1>{{sc.p + slot}}, red, s);
+    launch_reduce<1>(nown, Dot{a + off, b + off}, StoreTo<1>{{sc.p + slot}}, red, s);
+    if (sys.dist) sys.dist->comm.sum(sc.p + slot, 1, s);
   }
   double read(int slot) {
     double v = 0.0;
@@ -173,7 +202,8 @@ struct Ctx {
   }
   double true_res(const double* b, const double* x, double* tmp, double normb) {
     K(x, tmp);
-    launch_reduce<1>(nd, DiffSq{b, tmp}, StoreTo<1>{{sc.p + S_TR}}, red, s);
+    launch_reduce<1>(nown, DiffSq{b + off, tmp + off}, StoreTo<1>{{sc.p + S_TR}}, red, s);
+    if (sys.dist) sys.dist->comm.sum(sc.p + S_TR, 1, s);
     return std::sqrt(read(S_TR)) / normb;
   }
 };
@@ -224,7 +254,7 @@ void pcg_native(NativeSys& sys, const double* b, double* x, const SolverCfg& cfg
   for (int it = 0; it < cfg.maxiter; ++it) {
     C.K(p.p, q.p);
     C.dot(p.p, q.p, S_PQ);
-    launch_reduce<1>(nd, PcgStep{x, r, p.p, q.p, C.sc.p}, PcgStepPost{C.sc.p}, C.red, s);
+    C.reduce(PcgStep{x + C.off, r + C.off, p.p + C.off, q.p + C.off, C.sc.p}, PcgStepPost{C.sc.p}, S_TMP);
     double h[4];
     SG_CUDA(cudaMemcpyAsync(h, C.sc.p + S_PQ, 4 * sizeof(double), cudaMemcpyDeviceToHost, s));
     SG_CUDA(cudaStreamSynchronize(s));
@@ -252,7 +282,7 @@ void pcg_native(NativeSys& sys, const double* b, double* x, const SolverCfg& cfg
       target *= 0.1;
     }
     C.M(r, z.p);
-    launch_reduce<1>(nd, Dot{r, z.p}, RznPost{C.sc.p}, C.red, s);
+    C.reduce(Dot{r + C.off, z.p + C.off}, RznPost{C.sc.p}, S_TMP);
     pupd_kernel<<<nb256(nd), 256, 0, s>>>(nd, z.p, p.p, C.sc.p);
     SG_CHECK_LAUNCH();
   }
@@ -449,9 +479,19 @@ void fgmres_native(NativeSys& sys, const double* b, double* x, const SolverCfg& 
   out.wall_time = now() - t0;
 }
 
+// One slab-partitioned operator application on this rank's window vectors
+// (what 0: y = K_ktag x, what 1: y = M x).
+void dist_apply(NativeSys& sys, int what, const double* xw, double* yw, cudaStream_t s) {
+  SG_REQUIRE(sys.dist, "not a slab system");
+  Ctx C(sys, s);
+  if (what == 0) C.K(xw, yw);
+  else C.M(xw, yw);
+}
+
 // -------------------------------------------------------------- Lanczos
 void lanczos_native(NativeSys& sys, int m, uint64_t seed, std::vector<double>& H, int& used,
                     bool& partial, cudaStream_t s) {
+  SG_REQUIRE(!sys.dist, "the Lanczos probe is single-GPU");
   Ctx C(sys, s);
   const int64_t nd = C.nd;
   SG_REQUIRE(m >= 2 && m <= 200, "Lanczos steps out of range");

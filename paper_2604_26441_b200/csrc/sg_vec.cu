@@ -53,6 +53,18 @@ void build_grid(Grid& g, int nx, int ny, int nz, const uint8_t* dof_mask, cudaSt
   finish_grid(g, s);
 }
 
+// Slab window of a grid: node planes [k0, k1] (inclusive) of `full`, i.e. the
+// element layers [k0, k1) with the same Dirichlet bits (multi-GPU slabs).
+void build_window_grid(const Grid& full, int k0, int k1, Grid& w, cudaStream_t s) {
+  SG_REQUIRE(0 <= k0 && k0 < k1 && k1 <= full.d.nz, "bad slab window");
+  w.d.nx = full.d.nx;
+  w.d.ny = full.d.ny;
+  w.d.nz = k1 - k0;
+  const int64_t plane = int64_t(full.d.nx + 1) * (full.d.ny + 1);
+  w.h_nmask.assign(full.h_nmask.begin() + k0 * plane, full.h_nmask.begin() + (k1 + 1) * plane);
+  finish_grid(w, s);
+}
+
 // Injection: coarse DOF fixed iff fine DOF at node (2i,2j,2k) is (transfer.py:75-83).
 void build_coarse_grid(const Grid& fine, Grid& c, cudaStream_t s) {
   SG_REQUIRE(fine.d.nx % 2 == 0 && fine.d.ny % 2 == 0 && fine.d.nz % 2 == 0,
