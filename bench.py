@@ -160,7 +160,7 @@ def run_reference(args):
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": per_iter * 1e3, "higher_is_better": False, "scaling": "weak",
+        "ms_per_step": per_iter * 1e3, "higher_is_better": False, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64/f32 (FP32-GMG)", "data": "synthetic",
         "config": _config(args),
         "cpu_baseline": {"value": value, "unit": "s", "cores": os.cpu_count(), "kind": "port",
@@ -183,7 +183,8 @@ def _config(args):
     N = args.size
     return {"workload": f"{N}x{N}x{N} uniform rho=0.5 p=3 cantilever, FP32-GMG PCG (tol 1e-6, cap 200)",
             "elements": N ** 3, "levels_requested": 4, "policy": "fp32",
-            "parallelism": f"replicas x{args.gpus}" if args.gpus > 1 else "single GPU",
+            "parallelism": (f"z-slab partition x{args.gpus} (levels 0-1; NCCL halos + rank-ordered "
+                            "dot sums; coarse tail replicated)") if (args.gpus > 1 or args.slab) else "single GPU",
             "l2": "working set > 126 MB L2 (L1 operator 258 MB); L2 also flushed before each timed solve"}
 
 
@@ -195,8 +196,11 @@ def run_gpu(args):
 
     world, rank, local = _dist()
     torch.cuda.set_device(local)
-    if world > 1:
+    use_slab = world > 1 or args.slab
+    if use_slab:
         import torch.distributed as dist
+        if "MASTER_ADDR" not in os.environ:  # --slab on one process without torchrun
+            os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT="29533", RANK="0", WORLD_SIZE="1")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     import paper_2604_26441_b200 as P
     from paper_2604_26441_b200 import _dev, _native
@@ -217,9 +221,17 @@ def run_gpu(args):
     cfg = P.SolverConfig(tol=1e-6, maxiter=200)
     flush = torch.empty(256 * 2 ** 20 // 4, dtype=torch.float32, device="cuda")
     stream = torch.cuda.current_stream()
+    if use_slab:
+        # slab partition of levels 0-1 over the ranks (NCCL halos / dot sums),
+        # coarse tail replicated (paper_2604_26441_b200/slab.py)
+        from paper_2604_26441_b200.slab import SlabSolver
+        slab = SlabSolver(op, h)
+        solve = lambda b: slab.pcg(b, cfg)
+    else:
+        solve = lambda b: P.pcg(op.matvec, h.vcycle, b, cfg)
 
     for _ in range(args.warmup):
-        rep = P.pcg(op.matvec, h.vcycle, b_dev, cfg)
+        rep = solve(b_dev)
     torch.cuda.synchronize()
     if world > 1:
         torch.distributed.barrier()
@@ -232,7 +244,7 @@ def run_gpu(args):
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
             e0.record(stream)
-            rep = P.pcg(op.matvec, h.vcycle, b_dev, cfg)
+            rep = solve(b_dev)
             e1.record(stream)
             e1.synchronize()
             total_ms += e0.elapsed_time(e1)
@@ -255,11 +267,15 @@ def run_gpu(args):
         flush.zero_()
         torch.cuda.synchronize()
         s = time.perf_counter()
-        rep_h = P.pcg(op.matvec, h.vcycle, b_pin, cfg)
+        rep_h = solve(b_pin)
         x_pin.copy_(rep_h.x, non_blocking=False)
         torch.cuda.synchronize()
         e2e.append(time.perf_counter() - s)
     e2e_s = sum(e2e) / len(e2e)
+    if world > 1:
+        t = torch.tensor([e2e_s], device="cuda", dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        e2e_s = float(t.item())
     assert np.allclose(x_pin.numpy(), rep.x.cpu().numpy())
 
     # per-component device timings (CUDA events inside the library)
@@ -297,7 +313,7 @@ def run_gpu(args):
             traffic = None
     line = {
         "metric": METRIC, "value": ms / 1e3, "unit": "s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False, "scaling": "weak",
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False, "scaling": "strong",
         "vs_baseline": None, "dtype": "f32 (fine level) / f64 (coarse, outer PCG)",
         "data": "synthetic (uniform rho=0.5 cantilever, deterministic fixture)",
         "config": _config(args),
@@ -323,7 +339,7 @@ def run_gpu(args):
                                           f"{iters[-1]} iterations"}
     if rank == 0:
         print(json.dumps(line))
-    if world > 1:
+    if use_slab:
         torch.distributed.destroy_process_group()
     return 0
 
@@ -336,6 +352,7 @@ def main():
     ap.add_argument("--impl", default="native", choices=["native", "reference"])
     ap.add_argument("--size", type=int, default=100)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--slab", action="store_true", help="use the slab-partitioned path even on 1 GPU")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
