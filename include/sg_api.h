@@ -161,7 +161,8 @@ int sg_ptap_csr(int64_t nf, int64_t nc, const int64_t* Pp, const int64_t* Pj, co
                 int64_t* nnz, void* stream);
 int sg_csr_result_get(void* result, int64_t* Cp, int64_t* Cj, double* Cx);
 void sg_csr_result_free(void* result);
-/* Development instrumentation: pcg80 phase timestamps (ns) of block 0, step 10. */
+/* Development instrumentation: pcg80 phase timestamps (ns) of step 10, out[8*block + k]
+ * for every block (out: 8 x 256 int64; unused blocks 0). */
 int sg_hier_pcg80_trace(sg_hier* h, long long* out, void* stream);
 
 /* ---------------------------------------------------------------------

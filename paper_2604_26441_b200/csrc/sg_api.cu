@@ -740,13 +740,13 @@ extern "C" int sg_hier_pcg80_trace(sg_hier* h, long long* out, void* stream) {
     cudaStream_t s = S(stream);
     sg::Hier& H = *h->h;
     SG_REQUIRE(H.coarsest_mode == 1, "coarsest solver is not pcg80");
-    sg::DBuf<long long> t(16);
+    sg::DBuf<long long> t(8 * 256);
     t.zero(s);
     sg::Level& Lc = *H.lv.back();
     H.pcg.trace = t.p;
     sg::coarsest_solve(H, Lc.w.r.p, Lc.w.x.p, s);
     H.pcg.trace = nullptr;
-    t.download(out, 9, s);
+    t.download(out, 8 * 256, s);
     SG_CUDA(cudaStreamSynchronize(s));
   });
 }

@@ -6,7 +6,7 @@
 //    host.  Each block keeps its operator rows resident in shared memory for
 //    the whole solve; per step: phase A (q = (K+eps I) p with p = z + beta
 //    p_old recomputed for the neighbours on the fly, branch-free), a grid
-//    all-reduce (tree barrier + every block summing the block partials in
+//    all-reduce (counter barrier + every block summing the block partials in
 //    index order: deterministic), phase B (x, r, z updates) and a second
 //    all-reduce.
 //  * dense: Cholesky of K + eps*I computed on device at setup, then the
@@ -27,71 +27,74 @@ struct Pcg80Args {
   double* p0;
   double* p1;
   double* q;
-  double* partials;    // 2 * gridDim.x (double-buffered by epoch parity)
-  unsigned* bar;       // [0] root counter, [32] release flag, [64*(1+g)] group counters
+  double* partials;    // [2][gridDim.x] block partials (double-buffered by epoch parity)
+  unsigned* bar;       // monotonic arrival counter
   double eps;
   int steps;
   int cache_slots;     // stencil slots resident in shared memory (single-pass grids)
-  long long* trace;    // optional: %globaltimer stamps of block 0, step 10
+  long long* trace;    // optional: %globaltimer stamps of every block, step 10 (8 per block)
 };
 
 #define PCG_STAMP(k)                                                                  \
   do {                                                                                \
-    if (P.trace && s == 10 && blockIdx.x == 0 && threadIdx.x == 0) {                  \
+    if (P.trace && s == 10 && threadIdx.x == 0) {                                     \
       long long t_;                                                                   \
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                          \
-      P.trace[k] = t_;                                                                \
+      P.trace[blockIdx.x * 8 + k] = t_;                                               \
     }                                                                                 \
   } while (0)
 
 constexpr int kPcgNodes = 128;                 // nodes per block pass
 constexpr int kPcgThreads = 3 * kPcgNodes;     // one thread per (node, dk plane)
-constexpr int kBarGroup = 16;                  // blocks per first-level barrier group
 
-// Two-level arrival tree (groups of 16 blocks, then the group leaders) so no
-// counter sees more than 16-way atomic contention; the root releases a flag
-// that every block acquires.
-__device__ __forceinline__ void tree_barrier(unsigned* bar, unsigned epoch) {
-  // (measured: a flat monotonic counter beats both a 16-ary arrival tree and
-  // per-block flag polling on B200 at ~140 participants)
-  const unsigned target = epoch * gridDim.x;
-  asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(bar) : "memory");
-  unsigned f;
-  do {
-    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(f) : "l"(bar) : "memory");
-  } while (f < target);
+// Grid all-reduce: thread 0 of every block stores the block partial and
+// arrives on a monotonic counter with a release reduction, then spins with
+// acquire loads (one poller per block: polling every partial from every block
+// contends on the same L2 lines and was measured 2.5x slower).  After the
+// block barrier, threads 0..nb-1 load one partial each (a single L2 round
+// trip) and the totals are summed in a fixed tree over the block index: every
+// block obtains identical bits, independent of arrival order.
+__device__ __forceinline__ void stamp(long long* tr, int k) {
+  if (tr && threadIdx.x == 0) {
+    long long t_;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));
+    tr[blockIdx.x * 8 + k] = t_;
+  }
 }
 
-// Block partial (fixed shuffle tree + fixed warp order) -> partials; tree
-// barrier; every block sums all partials in index order (lane-strided +
-// fixed xor tree): identical totals on every block, deterministic.
 __device__ __forceinline__ double grid_allreduce(double v, const Pcg80Args& P, unsigned epoch,
-                                                 double* sm) {
+                                                 double* sm, long long* tr = nullptr) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nw = int(blockDim.x >> 5);
   if (lane == 0) sm[warp] = v;
   __syncthreads();
   const int nb = gridDim.x;
   double* part = P.partials + (epoch & 1) * nb;
-  if (threadIdx.x < 32) {
-    double s = lane < int(blockDim.x >> 5) ? sm[lane] : 0.0;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    if (lane == 0) {
-      __stcg(part + blockIdx.x, s);
-      tree_barrier(P.bar, epoch);
-    }
-    __syncwarp();
-    double t = 0.0;
-    for (int b = lane; b < nb; b += 32) t += __ldcg(part + b);
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
-    if (lane == 0) sm[0] = t;
+  if (threadIdx.x == 0) {
+    double s = sm[0];
+    for (int w = 1; w < nw; ++w) s += sm[w];
+    __stcg(part + blockIdx.x, s);
+    const unsigned target = epoch * unsigned(nb);
+    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(P.bar) : "memory");
+    stamp(tr, 5);
+    unsigned f;
+    do {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(f) : "l"(P.bar) : "memory");
+    } while (f < target);
+    stamp(tr, 6);
   }
   __syncthreads();
-  const double tot = sm[0];
+  double t = int(threadIdx.x) < nb ? __ldcg(part + threadIdx.x) : 0.0;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+  if (lane == 0) sm[warp] = t;
   __syncthreads();
+  double tot = sm[0];
+  for (int w = 1; w < nw; ++w) tot += sm[w];
+  __syncthreads();
+  stamp(tr, 7);
   return tot;
 }
 
@@ -197,7 +200,7 @@ __global__ void __launch_bounds__(kPcgThreads) pcg80_kernel(Pcg80Args P) {
       __syncthreads();
     }
     PCG_STAMP(1);
-    const double pq = grid_allreduce(loc, P, ++epoch, sm);
+    const double pq = grid_allreduce(loc, P, ++epoch, sm, (P.trace && s == 10) ? P.trace : nullptr);
     PCG_STAMP(2);
     if (!(pq > 0.0) || !isfinite(pq)) break;
     const double a = rz / pq;
@@ -261,7 +264,7 @@ void Pcg80::setup(const Grid& g, const double* A, const double* diag, double eps
   SG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pcg80_kernel, kPcgThreads, smem_bytes));
   SG_REQUIRE(per_sm >= 1, "pcg80 kernel cannot be resident");
   partials.alloc(size_t(2 * nblocks));
-  bar.alloc(size_t(64 * (2 + (nblocks + kBarGroup - 1) / kBarGroup)));
+  bar.alloc(32);
   SG_CUDA(cudaStreamSynchronize(s));
 }
 
