@@ -118,10 +118,10 @@ void level_apply(Hier& H, Level& L, int tag, const void* x, void* y, cudaStream_
     return;
   }
   if (tag == TAG_FP64) {
-    stencil_apply<double>(*L.g, L.st.A64.p, (const double*)x, (double*)y, s);
+    stencil_apply<double>(*L.g, L.st.T64.p, (const double*)x, (double*)y, s);
   } else if (tag == TAG_FP32) {
-    SG_REQUIRE(L.st.A32.p, "fp32 operator copy missing");
-    stencil_apply<float>(*L.g, L.st.A32.p, (const float*)x, (float*)y, s);
+    SG_REQUIRE(L.st.T32.p, "fp32 operator copy missing");
+    stencil_apply<float>(*L.g, L.st.T32.p, (const float*)x, (float*)y, s);
   } else {
     throw Error("bf16 tag on an assembled level is not produced by any policy");
   }
@@ -433,7 +433,9 @@ std::unique_ptr<Hier> hier_build(FineOp* fine, FineWork& fw, const HParams& p, c
       if (L.tag == TAG_FP32) {
         L.st.A32.alloc(size_t(243 * L.g->d.nnodes()));
         stencil_round_f32(*L.g, L.st.A64.p, L.st.A32.p, false, s);
+        stencil_tile<float>(*L.g, L.st.A32.p, L.st.T32, s);
       }
+      stencil_tile<double>(*L.g, L.st.A64.p, L.st.T64, s);
     }
     launch_ew(int64_t(n), s, [&](int nb, int nt) { recip_kernel<<<nb, nt, 0, s>>>(int64_t(n), L.diag.p, L.dinv.p, L.dinv32.p); });
     alloc_work(L);
@@ -598,7 +600,9 @@ std::unique_ptr<DistPart> dist_build(Hier& F, int n_dist, const int* planes, con
       if (FL.st.A32.p) {
         L->st.A32.alloc(size_t(243 * nnw));
         copy_planes(FL.st.A32.p, nnf, L->st.A32.p, nnw, off, 243, s);
+        stencil_tile<float>(L->own, L->st.A32.p, L->st.T32, s);
       }
+      stencil_tile<double>(L->own, L->st.A64.p, L->st.T64, s);
     }
     const int64_t n = 3 * L->g->d.nnodes();
     const int64_t voff = int64_t(D->w0[l]) * 3 * (FL.g->d.nx + 1) * (FL.g->d.ny + 1);

@@ -83,11 +83,16 @@ void transfer_export_csr(const Grid& fine, const Grid& coarse, int64_t* indptr, 
 struct Stencil {
   DBuf<double> A64;
   DBuf<float> A32;
+  DBuf<double> T64;  // tiled copies for the SpMV (stencil_tile)
+  DBuf<float> T32;
   int64_t nnz = 0;  // nonzero entries on free rows (CSR nnz of the reference)
 };
 
+// y = A x with At the tiled copy of A (stencil_tile)
 template <class T>
-void stencil_apply(const Grid& g, const T* A, const T* x, T* y, cudaStream_t s);
+void stencil_apply(const Grid& g, const T* At, const T* x, T* y, cudaStream_t s);
+template <class T>
+void stencil_tile(const Grid& g, const T* A, DBuf<T>& At, cudaStream_t s);
 void stencil_diag(const Grid& g, const double* A, double* d, cudaStream_t s);
 void stencil_round_f32(const Grid& g, const double* A64, float* A32, bool bf16, cudaStream_t s);
 void fine_to_stencil(const FineOp& op, double* A, cudaStream_t s);

@@ -25,36 +25,42 @@ __device__ __forceinline__ double add_rn<double>(double a, double b) { return __
 template <>
 __device__ __forceinline__ float add_rn<float>(float a, float b) { return __fadd_rn(a, b); }
 
+// Reads the TILED copy of the operator (stencil_tile: 32-node tiles, the 243
+// coefficients of a tile contiguous), so each warp streams one contiguous
+// 243 x 256 B block instead of 243 strided 256 B pieces (DRAM page locality).
+// Branch-free and fully unrolled: out-of-grid neighbours are clamped onto the
+// node itself, where the stored coefficients are exact zeros (the assembly
+// zero-fills every slot), so all 243 coefficient loads and 81 neighbour loads
+// of a row are independent and in flight together (the operator streams once
+// per apply: memory-level parallelism is the bound).  The summation order is
+// still the scipy csr_matvec order; a 0*x term only adds a signed zero.
 template <class T>
-__global__ void __launch_bounds__(128) stencil_apply_kernel(GridDesc g, const T* __restrict__ A,
+__global__ void __launch_bounds__(128) stencil_apply_kernel(GridDesc g, const T* __restrict__ At,
                                                             const T* __restrict__ x, T* __restrict__ y) {
   const int64_t nn = g.nnodes();
   const int64_t node = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (node >= nn) return;
   const int NX = g.nx + 1, NY = g.ny + 1;
-  const int i = int(node % NX), j = int((node / NX) % NY), k = int(node / (int64_t(NX) * NY));
+  const int64_t NXY = int64_t(NX) * NY;
+  const int i = int(node % NX), j = int((node / NX) % NY), k = int(node / NXY);
+  const int64_t oi[3] = {i > 0 ? -1 : 0, 0, i < g.nx ? 1 : 0};
+  const int64_t oj[3] = {j > 0 ? -NX : 0, 0, j < g.ny ? NX : 0};
+  const int64_t ok[3] = {k > 0 ? -NXY : 0, 0, k < g.nz ? NXY : 0};
   T s0 = 0, s1 = 0, s2 = 0;
-  for (int dk = -1; dk <= 1; ++dk) {
-    if (k + dk < 0 || k + dk > g.nz) continue;
-    for (int dj = -1; dj <= 1; ++dj) {
-      if (j + dj < 0 || j + dj > g.ny) continue;
-      for (int di = -1; di <= 1; ++di) {
-        if (i + di < 0 || i + di > g.nx) continue;
-        const int slot = (dk + 1) * 9 + (dj + 1) * 3 + (di + 1);
-        const int64_t nb = node + di + int64_t(NX) * (dj + int64_t(NY) * dk);
-        const T x0 = x[3 * nb], x1 = x[3 * nb + 1], x2 = x[3 * nb + 2];
-        const T* a = A + int64_t(slot) * 9 * nn + node;
-        s0 = add_rn(s0, mul_rn(a[0 * nn], x0));
-        s0 = add_rn(s0, mul_rn(a[1 * nn], x1));
-        s0 = add_rn(s0, mul_rn(a[2 * nn], x2));
-        s1 = add_rn(s1, mul_rn(a[3 * nn], x0));
-        s1 = add_rn(s1, mul_rn(a[4 * nn], x1));
-        s1 = add_rn(s1, mul_rn(a[5 * nn], x2));
-        s2 = add_rn(s2, mul_rn(a[6 * nn], x0));
-        s2 = add_rn(s2, mul_rn(a[7 * nn], x1));
-        s2 = add_rn(s2, mul_rn(a[8 * nn], x2));
-      }
-    }
+#pragma unroll
+  for (int slot = 0; slot < 27; ++slot) {
+    const int64_t nb = node + oi[slot % 3] + oj[(slot / 3) % 3] + ok[slot / 9];
+    const T x0 = x[3 * nb], x1 = x[3 * nb + 1], x2 = x[3 * nb + 2];
+    const T* a = At + (node >> 5) * (243 * 32) + slot * (9 * 32) + (node & 31);
+    s0 = add_rn(s0, mul_rn(__ldcs(a + 0 * 32), x0));
+    s0 = add_rn(s0, mul_rn(__ldcs(a + 1 * 32), x1));
+    s0 = add_rn(s0, mul_rn(__ldcs(a + 2 * 32), x2));
+    s1 = add_rn(s1, mul_rn(__ldcs(a + 3 * 32), x0));
+    s1 = add_rn(s1, mul_rn(__ldcs(a + 4 * 32), x1));
+    s1 = add_rn(s1, mul_rn(__ldcs(a + 5 * 32), x2));
+    s2 = add_rn(s2, mul_rn(__ldcs(a + 6 * 32), x0));
+    s2 = add_rn(s2, mul_rn(__ldcs(a + 7 * 32), x1));
+    s2 = add_rn(s2, mul_rn(__ldcs(a + 8 * 32), x2));
   }
   y[3 * node] = s0;
   y[3 * node + 1] = s1;
@@ -62,11 +68,31 @@ __global__ void __launch_bounds__(128) stencil_apply_kernel(GridDesc g, const T*
 }
 
 template <class T>
-void stencil_apply(const Grid& g, const T* A, const T* x, T* y, cudaStream_t s) {
+void stencil_apply(const Grid& g, const T* At, const T* x, T* y, cudaStream_t s) {
   const int64_t nn = g.d.nnodes();
-  stencil_apply_kernel<T><<<grid_blocks(nn, 128), 128, 0, s>>>(g.d, A, x, y);
+  stencil_apply_kernel<T><<<grid_blocks(nn, 128), 128, 0, s>>>(g.d, At, x, y);
   SG_CHECK_LAUNCH();
 }
+
+// At[(tile*243 + q)*32 + lane] = A[q*nn + tile*32 + lane] (zero padded)
+template <class T>
+__global__ void stencil_tile_kernel(int64_t nn, int64_t ntiles, const T* __restrict__ A,
+                                    T* __restrict__ At) {
+  const int64_t idx = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (idx >= ntiles * 243 * 32) return;
+  const int64_t lane = idx & 31, q = (idx >> 5) % 243, tile = (idx >> 5) / 243;
+  const int64_t node = tile * 32 + lane;
+  At[idx] = node < nn ? A[q * nn + node] : T(0);
+}
+template <class T>
+void stencil_tile(const Grid& g, const T* A, DBuf<T>& At, cudaStream_t s) {
+  const int64_t nn = g.d.nnodes(), nt = (nn + 31) / 32;
+  At.alloc(size_t(nt * 243 * 32));
+  stencil_tile_kernel<T><<<grid_blocks(nt * 243 * 32, 256), 256, 0, s>>>(nn, nt, A, At.p);
+  SG_CHECK_LAUNCH();
+}
+template void stencil_tile<double>(const Grid&, const double*, DBuf<double>&, cudaStream_t);
+template void stencil_tile<float>(const Grid&, const float*, DBuf<float>&, cudaStream_t);
 template void stencil_apply<double>(const Grid&, const double*, const double*, double*, cudaStream_t);
 template void stencil_apply<float>(const Grid&, const float*, const float*, float*, cudaStream_t);
 
