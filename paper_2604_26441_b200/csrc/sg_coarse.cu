@@ -62,6 +62,14 @@ __device__ __forceinline__ void stamp(long long* tr, int k) {
   }
 }
 
+// Sum of the per-warp values sm[0..nw) by one warp in a fixed xor tree.
+__device__ __forceinline__ double warp_sum_of(const double* sm, int nw, int lane) {
+  double v = lane < nw ? sm[lane] : 0.0;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
 __device__ __forceinline__ double grid_allreduce(double v, const Pcg80Args& P, unsigned epoch,
                                                  double* sm, long long* tr = nullptr) {
 #pragma unroll
@@ -72,28 +80,27 @@ __device__ __forceinline__ double grid_allreduce(double v, const Pcg80Args& P, u
   __syncthreads();
   const int nb = gridDim.x;
   double* part = P.partials + (epoch & 1) * nb;
-  if (threadIdx.x == 0) {
-    double s = sm[0];
-    for (int w = 1; w < nw; ++w) s += sm[w];
-    __stcg(part + blockIdx.x, s);
-    const unsigned target = epoch * unsigned(nb);
-    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(P.bar) : "memory");
-    stamp(tr, 5);
-    unsigned f;
-    do {
-      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(f) : "l"(P.bar) : "memory");
-    } while (f < target);
-    stamp(tr, 6);
+  if (warp == 0) {
+    const double s = warp_sum_of(sm, nw, lane);
+    if (lane == 0) {
+      __stcg(part + blockIdx.x, s);
+      const unsigned target = epoch * unsigned(nb);
+      asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(P.bar) : "memory");
+      stamp(tr, 5);
+      unsigned f;
+      do {
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(f) : "l"(P.bar) : "memory");
+      } while (f < target);
+      stamp(tr, 6);
+    }
   }
   __syncthreads();
   double t = int(threadIdx.x) < nb ? __ldcg(part + threadIdx.x) : 0.0;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
-  if (lane == 0) sm[warp] = t;
+  if (lane == 0) sm[16 + warp] = t;
   __syncthreads();
-  double tot = sm[0];
-  for (int w = 1; w < nw; ++w) tot += sm[w];
-  __syncthreads();
+  const double tot = warp_sum_of(sm + 16, nw, lane);
   stamp(tr, 7);
   return tot;
 }
@@ -102,7 +109,7 @@ __device__ __forceinline__ double grid_allreduce(double v, const Pcg80Args& P, u
 // bit-reproducible in the reference either (OpenBLAS ddot), so the SpMV here
 // uses FMA and independent row accumulators; reductions are deterministic.
 __global__ void __launch_bounds__(kPcgThreads) pcg80_kernel(Pcg80Args P) {
-  __shared__ double sm[kPcgThreads / 32];
+  __shared__ double sm[32];  // [0,16): block partials, [16,32): partial sums
   __shared__ double rowpart[2][kPcgNodes][3];
   extern __shared__ double smA[];  // [cache_slots*9][kPcgNodes] operator rows of this block
   const int64_t nn = P.g.nnodes();
