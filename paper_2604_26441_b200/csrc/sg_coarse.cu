@@ -12,6 +12,7 @@
 //  * dense: Cholesky of K + eps*I computed on device at setup, then the
 //    explicit inverse, so each V-cycle's coarsest solve is one GEMV.
 #include <cmath>
+#include <cstdlib>
 #include "sg_coarse.cuh"
 
 namespace sg {
@@ -231,6 +232,312 @@ __global__ void __launch_bounds__(kPcgThreads) pcg80_kernel(Pcg80Args P) {
   }
 }
 
+// ------------------------------------------------------------ brick pcg80
+// Same algorithm, data-parallel over 3D node bricks (one brick per block,
+// one block per SM) instead of contiguous node ranges:
+//  * the operator rows stay on chip for all steps: the dj = -1 stencil row of
+//    each thread's dk plane in registers (27 doubles), the other 18 slots in
+//    shared memory (the full operator does not fit in 227 KB);
+//  * p lives in shared memory on the brick plus a one-node halo and is
+//    updated there, p = z + beta p, for halo nodes too (the same expression
+//    on the same bits as the owner's), so z is the only vector that crosses
+//    blocks;
+//  * z crosses blocks as 16-byte LL packets {lo, flag, hi, flag}: each 8-byte
+//    half carries the writer's step flag, so a reader knows the value is
+//    current without a memory fence (fences measured ~0.7 us each on B200);
+//  * the owner thread of a node keeps x, r, D^-1, q of its node in registers;
+//  * each grid all-reduce: block partial -> LL packet, relaxed arrival on a
+//    64-bit counter, one poller, then warp 0 reads all packets (validated by
+//    flag) and sums them in a fixed order: identical bits on every block.
+//    Flags carry a launch sequence kept on device, so CUDA-graph replays never
+//    accept a stale packet.
+constexpr int kBrCap = 144;                  // max nodes per brick
+constexpr int kBrThreads = 3 * kBrCap;       // one thread per (node, dk plane)
+constexpr int kBrRegRows = 3;                // q9 = 0..2 (dj = -1) kept in registers
+constexpr int kBrSmRows = 9 - kBrRegRows;
+constexpr int kBrWinMax = 640;               // halo-window nodes
+constexpr int kBrSmemA = 3 * kBrSmRows * 9 * kBrCap;  // doubles
+constexpr int kBrFill = (3 * kBrWinMax + kBrThreads - 1) / kBrThreads;
+
+struct BrickState {           // device-resident across launches (Pcg80::bstate)
+  unsigned long long count;   // arrival counter (monotonic)
+  unsigned long long origin;  // counter value when the next launch starts
+  unsigned long long seq;     // launch sequence
+};
+
+struct BrickArgs {
+  GridDesc g;
+  const double* A;     // stencil SoA (243 * nn)
+  const double* dinv;  // node layout, 0 on fixed
+  const double* b;     // node layout
+  double* x;           // node layout
+  uint4* zll;          // [3][nn] LL packets of z
+  uint4* slots;        // [2][gridDim.x] LL packets of block partials
+  BrickState* st;
+  double eps;
+  int steps;
+  int sx, sy, sz;
+  long long* trace;
+};
+
+__device__ __forceinline__ void ll_store(uint4* a, double v, unsigned flag) {
+  asm volatile("st.volatile.global.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(a),
+               "r"(unsigned(__double2loint(v))), "r"(flag), "r"(unsigned(__double2hiint(v))),
+               "r"(flag) : "memory");
+}
+__device__ __forceinline__ bool ll_load(const uint4* a, unsigned flag, double& v) {
+  unsigned lo, f0, hi, f1;
+  asm volatile("ld.volatile.global.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(lo), "=r"(f0), "=r"(hi), "=r"(f1) : "l"(a) : "memory");
+  v = __hiloint2double(int(hi), int(lo));
+  return f0 == flag && f1 == flag;
+}
+
+__device__ __forceinline__ double wsum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+__device__ __forceinline__ double br_allreduce(double v, const BrickArgs& P, unsigned flag,
+                                               unsigned long long target, double* red,
+                                               double* tot) {
+  v = wsum(v);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  if (warp == 0) {
+    const int nb = gridDim.x;
+    uint4* sl = P.slots + (flag & 1) * nb;
+    const double s = wsum(lane < int(blockDim.x >> 5) ? red[lane] : 0.0);
+    if (lane == 0) {
+      ll_store(sl + blockIdx.x, s, flag);
+      asm volatile("red.relaxed.gpu.global.add.u64 [%0], 1;" ::"l"(&P.st->count) : "memory");
+      unsigned long long c;
+      do {
+        asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(c) : "l"(&P.st->count) : "memory");
+      } while (c < target);
+    }
+    __syncwarp();
+    double acc[5];
+    bool ok;
+    do {
+      ok = true;
+#pragma unroll
+      for (int k = 0; k < 5; ++k) {
+        const int bb = lane + 32 * k;
+        acc[k] = 0.0;
+        if (bb < nb) ok = ll_load(sl + bb, flag, acc[k]) && ok;
+      }
+    } while (!__all_sync(0xffffffffu, ok));
+    const double t = wsum(acc[0] + acc[1] + acc[2] + acc[3] + acc[4]);
+    if (lane == 0) *tot = t;
+  }
+  __syncthreads();
+  return *tot;
+}
+
+__global__ void __launch_bounds__(kBrThreads, 1) pcg80_brick_kernel(BrickArgs P) {
+  extern __shared__ double smdyn[];
+  double* smA = smdyn;             // [(part*6 + row)*9 + entry][kBrCap]
+  double* pw = smdyn + kBrSmemA;   // [3][kBrWinMax] p on the brick + halo
+  __shared__ double rowpart[2][3][kBrCap];
+  __shared__ double red[32];
+  __shared__ double tot;
+  const int NX = P.g.nx + 1, NY = P.g.ny + 1, NZ = P.g.nz + 1;
+  const int nn = NX * NY * NZ;
+  const int bxi = int(blockIdx.x) % P.sx, byi = (int(blockIdx.x) / P.sx) % P.sy,
+            bzi = int(blockIdx.x) / (P.sx * P.sy);
+  const int x0 = bxi * NX / P.sx, y0 = byi * NY / P.sy, z0 = bzi * NZ / P.sz;
+  const int bx = (bxi + 1) * NX / P.sx - x0, by = (byi + 1) * NY / P.sy - y0,
+            bz = (bzi + 1) * NZ / P.sz - z0;
+  const int nloc = bx * by * bz;
+  const int WX = bx + 2, WY = by + 2, WZ = bz + 2, wn = WX * WY * WZ;
+  const int t = threadIdx.x;
+  const int part = t / kBrCap, ln = t % kBrCap;
+  const bool act = ln < nloc;
+  const int lnc = act ? ln : 0;
+  const int lx = lnc % bx, ly = (lnc / bx) % by, lz = lnc / (bx * by);
+  const int node = (x0 + lx) + NX * ((y0 + ly) + NY * (z0 + lz));
+  const bool owner = part == 0 && act;
+  const int nb = gridDim.x;
+
+  // launch sequence and counter origin (written by block 0 at the end of the
+  // previous launch; every block reads them before its first arrival)
+  const unsigned seq = unsigned(__ldcg(&P.st->seq));
+  const unsigned long long c0 = __ldcg(&P.st->origin);
+  const unsigned fbase = (seq + 1u) << 10;
+
+  // operator rows: dj = -1 row of this thread's dk plane in registers, the
+  // rest in shared memory
+  double areg[kBrRegRows * 9];
+#pragma unroll
+  for (int q = 0; q < kBrRegRows * 9; ++q)
+    areg[q] = act ? __ldg(P.A + int64_t((part * 9 + q / 9) * 9 + q % 9) * nn + node) : 0.0;
+  for (int idx = t; idx < kBrSmemA; idx += blockDim.x) {
+    const int e = idx / kBrCap, l = idx % kBrCap;
+    const int pp = e / (kBrSmRows * 9), qq = (e / 9) % kBrSmRows, ent = e % 9;
+    double v = 0.0;
+    if (l < nloc) {
+      const int gx = x0 + l % bx, gy = y0 + (l / bx) % by, gz = z0 + l / (bx * by);
+      const int gn = gx + NX * (gy + NY * gz);
+      v = __ldg(P.A + int64_t((pp * 9 + kBrRegRows + qq) * 9 + ent) * nn + gn);
+    }
+    smA[idx] = v;
+  }
+  // halo-window cells this thread stages each step (fixed for the launch)
+  int fw[kBrFill], fg[kBrFill];
+#pragma unroll
+  for (int k = 0; k < kBrFill; ++k) {
+    const int iw = t + k * kBrThreads;
+    fw[k] = -1;
+    fg[k] = -1;
+    if (iw < 3 * wn) {
+      const int c = iw / wn, w = iw - c * wn;
+      const int wx = w % WX, wy = (w / WX) % WY, wz = w / (WX * WY);
+      const int gx = x0 - 1 + wx, gy = y0 - 1 + wy, gz = z0 - 1 + wz;
+      fw[k] = c * kBrWinMax + w;
+      if (gx >= 0 && gx < NX && gy >= 0 && gy < NY && gz >= 0 && gz < NZ)
+        fg[k] = c * nn + gx + NX * (gy + NY * gz);
+    }
+  }
+
+  // x = 0; r = b; z = dinv*r; p = z; rz = r.z
+  double xr[3] = {0.0, 0.0, 0.0}, rr[3] = {0.0, 0.0, 0.0}, dv[3] = {0.0, 0.0, 0.0};
+  double pown[3] = {0.0, 0.0, 0.0}, qown[3] = {0.0, 0.0, 0.0};
+  double loc = 0.0;
+  if (owner) {
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      rr[c] = P.b[3 * node + c];
+      dv[c] = P.dinv[3 * node + c];
+      const double zv = dv[c] * rr[c];
+      ll_store(P.zll + c * nn + node, zv, fbase);
+      loc = fma(rr[c], zv, loc);
+    }
+  }
+  unsigned epoch = 0;
+  ++epoch;
+  double rz = br_allreduce(loc, P, fbase | epoch, c0 + epoch * nb, red, &tot);
+  double beta = 0.0;
+  const int wbase = ((lz + part) * WY + ly) * WX + lx;
+  const int wctr = ((lz + 1) * WY + ly + 1) * WX + lx + 1;
+  for (int s = 0; s < P.steps; ++s) {
+    if (P.trace && s == 10) stamp(P.trace, 0);
+    // p = z + beta p on the brick + halo (z of step s carries flag fbase + s)
+    {
+      const unsigned zf = fbase + unsigned(s);
+      double zv[kBrFill];
+      bool ok[kBrFill];
+#pragma unroll
+      for (int k = 0; k < kBrFill; ++k) {
+        zv[k] = 0.0;
+        ok[k] = fg[k] < 0 || ll_load(P.zll + fg[k], zf, zv[k]);
+      }
+#pragma unroll
+      for (int k = 0; k < kBrFill; ++k)
+        while (!ok[k]) ok[k] = ll_load(P.zll + fg[k], zf, zv[k]);
+#pragma unroll
+      for (int k = 0; k < kBrFill; ++k)
+        if (fw[k] >= 0) pw[fw[k]] = s > 0 ? fma(beta, pw[fw[k]], zv[k]) : zv[k];
+    }
+    __syncthreads();
+    // q = (K + eps I) p
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+#pragma unroll
+    for (int q9 = 0; q9 < 9; ++q9) {
+      const int w = wbase + (q9 / 3) * WX + q9 % 3;
+      const double pv0 = pw[w], pv1 = pw[kBrWinMax + w], pv2 = pw[2 * kBrWinMax + w];
+      double a[9];
+#pragma unroll
+      for (int e = 0; e < 9; ++e)
+        a[e] = q9 < kBrRegRows ? areg[q9 * 9 + e]
+                               : smA[((part * kBrSmRows + q9 - kBrRegRows) * 9 + e) * kBrCap + ln];
+      a0 = fma(a[0], pv0, a0);
+      a0 = fma(a[1], pv1, a0);
+      a0 = fma(a[2], pv2, a0);
+      a1 = fma(a[3], pv0, a1);
+      a1 = fma(a[4], pv1, a1);
+      a1 = fma(a[5], pv2, a1);
+      a2 = fma(a[6], pv0, a2);
+      a2 = fma(a[7], pv1, a2);
+      a2 = fma(a[8], pv2, a2);
+    }
+    if (part > 0) {
+      rowpart[part - 1][0][ln] = a0;
+      rowpart[part - 1][1][ln] = a1;
+      rowpart[part - 1][2][ln] = a2;
+    }
+    __syncthreads();
+    loc = 0.0;
+    if (owner) {
+      const double av[3] = {a0 + rowpart[0][0][ln] + rowpart[1][0][ln],
+                            a1 + rowpart[0][1][ln] + rowpart[1][1][ln],
+                            a2 + rowpart[0][2][ln] + rowpart[1][2][ln]};
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        pown[c] = pw[c * kBrWinMax + wctr];
+        qown[c] = fma(P.eps, pown[c], av[c]);
+        loc = fma(pown[c], qown[c], loc);
+      }
+    }
+    if (P.trace && s == 10) stamp(P.trace, 1);
+    ++epoch;
+    const double pq = br_allreduce(loc, P, fbase | epoch, c0 + epoch * nb, red, &tot);
+    if (P.trace && s == 10) stamp(P.trace, 2);
+    if (!(pq > 0.0) || !isfinite(pq)) break;
+    const double al = rz / pq;
+    // x += a p; r -= a q; z = dinv r
+    loc = 0.0;
+    if (owner) {
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        xr[c] = fma(al, pown[c], xr[c]);
+        rr[c] = fma(-al, qown[c], rr[c]);
+        const double zv = dv[c] * rr[c];
+        ll_store(P.zll + c * nn + node, zv, fbase + unsigned(s) + 1u);
+        loc = fma(rr[c], zv, loc);
+      }
+    }
+    if (P.trace && s == 10) stamp(P.trace, 3);
+    ++epoch;
+    const double rzn = br_allreduce(loc, P, fbase | epoch, c0 + epoch * nb, red, &tot);
+    if (P.trace && s == 10) stamp(P.trace, 4);
+    if (!(rzn > 0.0) || !isfinite(rzn)) break;
+    beta = rzn / rz;
+    rz = rzn;
+  }
+  if (owner) {
+#pragma unroll
+    for (int c = 0; c < 3; ++c) P.x[3 * node + c] = xr[c];
+  }
+  if (blockIdx.x == 0 && t == 0) {
+    // every block arrived at all `epoch` all-reduces before block 0 left the last one
+    P.st->origin = c0 + (unsigned long long)epoch * nb;
+    P.st->seq = seq + 1u;
+  }
+}
+
+// Brick split of the node grid for pcg80_brick_kernel: at most nsm bricks of
+// at most kBrCap nodes, halo window <= kBrWinMax; smallest largest brick,
+// then smallest window.  false = no such split (use the range kernel).
+static bool brick_plan(const GridDesc& g, int nsm, int& sx, int& sy, int& sz) {
+  const int NX = g.nx + 1, NY = g.ny + 1, NZ = g.nz + 1;
+  long best_b = 1L << 40, best_w = 1L << 40;
+  bool found = false;
+  for (int a = 1; a <= std::min(NX, nsm); ++a)
+    for (int b = 1; a * b <= nsm && b <= NY; ++b)
+      for (int c = 1; a * b * c <= nsm && c <= NZ; ++c) {
+        const long ex = (NX + a - 1) / a, ey = (NY + b - 1) / b, ez = (NZ + c - 1) / c;
+        const long vol = ex * ey * ez, win = (ex + 2) * (ey + 2) * (ez + 2);
+        if (vol > kBrCap || win > kBrWinMax) continue;
+        if (vol < best_b || (vol == best_b && win < best_w)) {
+          best_b = vol; best_w = win; sx = a; sy = b; sz = c; found = true;
+        }
+      }
+  return found;
+}
+
 void Pcg80::setup(const Grid& g, const double* A, const double* diag, double eps_, int steps_,
                   cudaStream_t s) {
   grid = &g;
@@ -257,6 +564,27 @@ void Pcg80::setup(const Grid& g, const double* A, const double* diag, double eps
   SG_CUDA(cudaGetDevice(&dev));
   SG_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
   SG_CUDA(cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+  if (!getenv("SG_PCG80_RANGE") && brick_plan(g.d, nsm, sx, sy, sz)) {
+    brick = true;
+    nblocks = sx * sy * sz;
+    smem_bytes = int(sizeof(double)) * (kBrSmemA + 3 * kBrWinMax);
+    SG_REQUIRE(smem_bytes <= smem_optin, "pcg80 brick kernel shared memory");
+    SG_REQUIRE(2 * steps_ + 1 < 1024, "pcg80 step count too large for the packet flags");
+    SG_CUDA(cudaFuncSetAttribute(pcg80_brick_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 smem_bytes));
+    SG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pcg80_brick_kernel, kBrThreads,
+                                                          smem_bytes));
+    SG_REQUIRE(per_sm >= 1, "pcg80 brick kernel cannot be resident");
+    slots.alloc(size_t(2 * nblocks));
+    slots.zero(s);
+    zll.alloc(size_t(3 * g.d.nnodes()));
+    zll.zero(s);
+    bstate.alloc(3);
+    bstate.zero(s);
+    SG_CUDA(cudaStreamSynchronize(s));
+    return;
+  }
+  brick = false;
   const int64_t want = (g.d.nnodes() + kPcgNodes - 1) / kPcgNodes;
   // one block per SM: the barrier cost grows with the participant count, and a
   // single pass lets every block keep its operator rows in shared memory
@@ -276,6 +604,28 @@ void Pcg80::setup(const Grid& g, const double* A, const double* diag, double eps
 }
 
 void Pcg80::solve(const double* b, double* x, cudaStream_t s) {
+  if (brick) {
+    BrickArgs a;
+    a.g = grid->d;
+    a.A = Aptr;
+    a.dinv = dinv.p;
+    a.b = b;
+    a.x = x;
+    a.zll = zll.p;
+    a.slots = slots.p;
+    a.st = reinterpret_cast<BrickState*>(bstate.p);
+    a.eps = eps;
+    a.steps = steps;
+    a.sx = sx;
+    a.sy = sy;
+    a.sz = sz;
+    a.trace = trace;
+    void* args[] = {&a};
+    SG_CUDA(cudaLaunchCooperativeKernel((void*)pcg80_brick_kernel, dim3(nblocks), dim3(kBrThreads),
+                                        args, size_t(smem_bytes), s));
+    SG_CHECK_LAUNCH();
+    return;
+  }
   Pcg80Args a;
   a.g = grid->d;
   a.A = Aptr;

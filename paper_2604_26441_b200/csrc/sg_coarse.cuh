@@ -15,6 +15,11 @@ struct Pcg80 {
   int smem_bytes = 0;
   DBuf<double> dinv, r, z, p0, p1, q, partials;
   DBuf<unsigned> bar;
+  // brick-partitioned kernel (pcg80_brick_kernel) when the level fits on chip
+  bool brick = false;
+  int sx = 0, sy = 0, sz = 0;
+  DBuf<uint4> slots, zll;
+  DBuf<unsigned long long> bstate;
   void setup(const Grid& g, const double* A, const double* diag, double eps, int steps,
              cudaStream_t s);
   void solve(const double* b, double* x, cudaStream_t s);

@@ -230,3 +230,31 @@ def test_config1_40cube_fp32_gmg_golden():
     assert rep.iterations == int(z["iters"][0]) == 11
     np.testing.assert_allclose(rep.residual_history, z["hist"], rtol=1e-4)
     np.testing.assert_allclose(op.compliance(rep.x), float(z["compliance"][0]), rtol=1e-6)
+
+
+@pytest.mark.parametrize("dims,kind", [((24, 16, 12), "binary"), ((20, 20, 20), "uniform")])
+def test_pcg80_brick_vs_oracle(dims, kind):
+    """Coarsest pcg80 on a many-brick split (hierarchy.py:139-162) against the oracle."""
+    g, op, og, E, ke = _pair(dims, kind)
+    h = P.build_hierarchy(op, 3, "fp64", cholesky_cutoff=0)
+    oh = O.Hier(og, E, ke, 3, "fp64", cutoff=0)
+    assert h.coarsest.mode == oh.mode == "pcg80"
+    r = P.SplitMix64(11).gaussian(g.n_free)
+    assert _rel(h.vcycle(r), oh.vcycle(r)) < 1e-9
+
+
+def test_pcg80_brick_matches_range_kernel_100cube(monkeypatch):
+    """configs[3] coarsest level (26^3 nodes, 50,700 DOFs): the brick-partitioned
+    kernel and the contiguous-range kernel solve the same fixed 80-step PCG."""
+    N = 100
+    g = P.build_cantilever(N, N, N)
+    op = P.FineOperator(g, P.simp_modulus(P.make_state("uniform", N, N, N, vf=0.5), 3.0))
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        hb = P.build_hierarchy(op, 4, "fp32")
+        monkeypatch.setenv("SG_PCG80_RANGE", "1")
+        hr = P.build_hierarchy(op, 4, "fp32")
+    r = P.SplitMix64(5).gaussian(g.n_free)
+    zb, zr = hb.vcycle(r), hr.vcycle(r)
+    assert _rel(zb, zr) < 1e-9
+    np.testing.assert_array_equal(zb, hb.vcycle(r))  # replay-deterministic
