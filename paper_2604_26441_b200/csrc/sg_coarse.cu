@@ -337,6 +337,71 @@ __device__ __forceinline__ double br_allreduce(double v, const BrickArgs& P, uns
   return *tot;
 }
 
+// Two values in one all-reduce (the Chronopoulos-Gear step's (r.z, w.z)).
+__device__ __forceinline__ void br_allreduce2(double v0, double v1, const BrickArgs& P,
+                                              unsigned flag, unsigned long long target,
+                                              double* red, double* tot, double& t0, double& t1) {
+  v0 = wsum(v0);
+  v1 = wsum(v1);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) {
+    red[warp] = v0;
+    red[16 + warp] = v1;
+  }
+  __syncthreads();
+  if (warp == 0) {
+    const int nb = gridDim.x;
+    uint4* sl = P.slots + (flag & 1) * 2 * nb;
+    const int nw = int(blockDim.x >> 5);
+    const double s0 = wsum(lane < nw ? red[lane] : 0.0);
+    const double s1 = wsum(lane < nw ? red[16 + lane] : 0.0);
+    if (lane == 0) {
+      ll_store(sl + blockIdx.x, s0, flag);
+      ll_store(sl + nb + blockIdx.x, s1, flag);
+      asm volatile("red.relaxed.gpu.global.add.u64 [%0], 1;" ::"l"(&P.st->count) : "memory");
+      unsigned long long c;
+      do {
+        asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(c) : "l"(&P.st->count) : "memory");
+      } while (c < target);
+    }
+    __syncwarp();
+    double a0[5], a1[5];
+    bool ok;
+    do {
+      ok = true;
+#pragma unroll
+      for (int k = 0; k < 5; ++k) {
+        const int bb = lane + 32 * k;
+        a0[k] = 0.0;
+        a1[k] = 0.0;
+        if (bb < nb) {
+          ok = ll_load(sl + bb, flag, a0[k]) && ok;
+          ok = ll_load(sl + nb + bb, flag, a1[k]) && ok;
+        }
+      }
+    } while (!__all_sync(0xffffffffu, ok));
+    const double r0 = wsum(a0[0] + a0[1] + a0[2] + a0[3] + a0[4]);
+    const double r1 = wsum(a1[0] + a1[1] + a1[2] + a1[3] + a1[4]);
+    if (lane == 0) {
+      tot[0] = r0;
+      tot[1] = r1;
+    }
+  }
+  __syncthreads();
+  t0 = tot[0];
+  t1 = tot[1];
+}
+
+// kCG = false: the reference's Hestenes-Stiefel recurrence (two all-reduces
+// per step).  kCG = true: the Chronopoulos-Gear form of the same Jacobi-PCG
+// (identical iterates in exact arithmetic; one all-reduce of (r.z, w.z) per
+// step with w = (K + eps I) z and s = A p carried by recurrence):
+//   gamma = r.z, delta = w.z;  beta = gamma/gamma_prev;
+//   p.Ap = delta - beta*gamma/alpha_prev;  alpha = gamma/p.Ap;
+//   p = z + beta p; s = w + beta s; x += alpha p; r -= alpha s; z = D^-1 r.
+// The reference's break tests map one to one: its rz_new test of step i-1 is
+// the gamma test of step i, its p.q test the p.Ap test.
+template <bool kCG>
 __global__ void __launch_bounds__(kBrThreads, 1) pcg80_brick_kernel(BrickArgs P) {
   extern __shared__ double smdyn[];
   double* smA = smdyn;             // [(part*6 + row)*9 + entry][kBrCap]
@@ -344,6 +409,7 @@ __global__ void __launch_bounds__(kBrThreads, 1) pcg80_brick_kernel(BrickArgs P)
   __shared__ double rowpart[2][3][kBrCap];
   __shared__ double red[32];
   __shared__ double tot;
+  __shared__ double tot2[2];
   const int NX = P.g.nx + 1, NY = P.g.ny + 1, NZ = P.g.nz + 1;
   const int nn = NX * NY * NZ;
   const int bxi = int(blockIdx.x) % P.sx, byi = (int(blockIdx.x) / P.sx) % P.sy,
@@ -402,47 +468,37 @@ __global__ void __launch_bounds__(kBrThreads, 1) pcg80_brick_kernel(BrickArgs P)
     }
   }
 
-  // x = 0; r = b; z = dinv*r; p = z; rz = r.z
-  double xr[3] = {0.0, 0.0, 0.0}, rr[3] = {0.0, 0.0, 0.0}, dv[3] = {0.0, 0.0, 0.0};
-  double pown[3] = {0.0, 0.0, 0.0}, qown[3] = {0.0, 0.0, 0.0};
-  double loc = 0.0;
-  if (owner) {
-#pragma unroll
-    for (int c = 0; c < 3; ++c) {
-      rr[c] = P.b[3 * node + c];
-      dv[c] = P.dinv[3 * node + c];
-      const double zv = dv[c] * rr[c];
-      ll_store(P.zll + c * nn + node, zv, fbase);
-      loc = fma(rr[c], zv, loc);
-    }
-  }
-  unsigned epoch = 0;
-  ++epoch;
-  double rz = br_allreduce(loc, P, fbase | epoch, c0 + epoch * nb, red, &tot);
-  double beta = 0.0;
   const int wbase = ((lz + part) * WY + ly) * WX + lx;
   const int wctr = ((lz + 1) * WY + ly + 1) * WX + lx + 1;
-  for (int s = 0; s < P.steps; ++s) {
-    if (P.trace && s == 10) stamp(P.trace, 0);
-    // p = z + beta p on the brick + halo (z of step s carries flag fbase + s)
-    {
-      const unsigned zf = fbase + unsigned(s);
-      double zv[kBrFill];
-      bool ok[kBrFill];
+  // stage the halo window of the LL vector written with flag zf; out-of-grid
+  // cells are 0.  kAxpy: pw = beta*pw + v (p window), else pw = v.
+  auto fill = [&](unsigned zf, bool axpy, double beta) {
+    double zv[kBrFill];
+    bool ok[kBrFill];
+#pragma unroll
+    for (int k = 0; k < kBrFill; ++k) {
+      zv[k] = 0.0;
+      ok[k] = fg[k] < 0 || ll_load(P.zll + fg[k], zf, zv[k]);
+    }
+    // not yet written (the neighbour is still finishing its step): re-poll
+    // every pending cell together, one L2 round trip per pass
+    bool all = true;
+#pragma unroll
+    for (int k = 0; k < kBrFill; ++k) all = all && ok[k];
+    while (!all) {
+      all = true;
 #pragma unroll
       for (int k = 0; k < kBrFill; ++k) {
-        zv[k] = 0.0;
-        ok[k] = fg[k] < 0 || ll_load(P.zll + fg[k], zf, zv[k]);
+        if (!ok[k]) ok[k] = ll_load(P.zll + fg[k], zf, zv[k]);
+        all = all && ok[k];
       }
-#pragma unroll
-      for (int k = 0; k < kBrFill; ++k)
-        while (!ok[k]) ok[k] = ll_load(P.zll + fg[k], zf, zv[k]);
-#pragma unroll
-      for (int k = 0; k < kBrFill; ++k)
-        if (fw[k] >= 0) pw[fw[k]] = s > 0 ? fma(beta, pw[fw[k]], zv[k]) : zv[k];
     }
-    __syncthreads();
-    // q = (K + eps I) p
+#pragma unroll
+    for (int k = 0; k < kBrFill; ++k)
+      if (fw[k] >= 0) pw[fw[k]] = axpy ? fma(beta, pw[fw[k]], zv[k]) : zv[k];
+  };
+  // y = K v on the window (the three dk planes summed by the owner thread)
+  auto spmv = [&](double av[3]) {
     double a0 = 0.0, a1 = 0.0, a2 = 0.0;
 #pragma unroll
     for (int q9 = 0; q9 < 9; ++q9) {
@@ -469,11 +525,107 @@ __global__ void __launch_bounds__(kBrThreads, 1) pcg80_brick_kernel(BrickArgs P)
       rowpart[part - 1][2][ln] = a2;
     }
     __syncthreads();
+    av[0] = a0 + rowpart[0][0][ln] + rowpart[1][0][ln];
+    av[1] = a1 + rowpart[0][1][ln] + rowpart[1][1][ln];
+    av[2] = a2 + rowpart[0][2][ln] + rowpart[1][2][ln];
+  };
+
+  if constexpr (kCG) {
+    double xr[3] = {0.0, 0.0, 0.0}, rr[3] = {0.0, 0.0, 0.0}, dv[3] = {0.0, 0.0, 0.0};
+    double pp[3] = {0.0, 0.0, 0.0}, ss[3] = {0.0, 0.0, 0.0};
+    if (owner) {
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        rr[c] = P.b[3 * node + c];
+        dv[c] = P.dinv[3 * node + c];
+        ll_store(P.zll + c * nn + node, dv[c] * rr[c], fbase);
+      }
+    }
+    unsigned epoch = 0;
+    double gprev = 0.0, aprev = 0.0;
+    for (int s = 0; s < P.steps; ++s) {
+      if (P.trace && s == 10) stamp(P.trace, 0);
+      fill(fbase + unsigned(s), false, 0.0);
+      __syncthreads();
+      if (P.trace && s == 10) stamp(P.trace, 5);
+      double av[3];
+      spmv(av);
+      double lg = 0.0, ld = 0.0, zo[3] = {0.0, 0.0, 0.0}, wo[3] = {0.0, 0.0, 0.0};
+      if (owner) {
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          zo[c] = pw[c * kBrWinMax + wctr];
+          wo[c] = fma(P.eps, zo[c], av[c]);
+          lg = fma(rr[c], zo[c], lg);
+          ld = fma(wo[c], zo[c], ld);
+        }
+      }
+      if (P.trace && s == 10) stamp(P.trace, 1);
+      ++epoch;
+      double gam, del;
+      br_allreduce2(lg, ld, P, fbase | epoch, c0 + epoch * nb, red, tot2, gam, del);
+      if (P.trace && s == 10) stamp(P.trace, 2);
+      double beta = 0.0, pap = del;
+      if (s > 0) {
+        if (!(gam > 0.0) || !isfinite(gam)) break;
+        beta = gam / gprev;
+        pap = del - beta * gam / aprev;
+      }
+      if (!(pap > 0.0) || !isfinite(pap)) break;
+      const double al = gam / pap;
+      if (owner) {
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          pp[c] = fma(beta, pp[c], zo[c]);
+          ss[c] = fma(beta, ss[c], wo[c]);
+          xr[c] = fma(al, pp[c], xr[c]);
+          rr[c] = fma(-al, ss[c], rr[c]);
+          if (s + 1 < P.steps) ll_store(P.zll + c * nn + node, dv[c] * rr[c], fbase + unsigned(s) + 1u);
+        }
+      }
+      if (P.trace && s == 10) stamp(P.trace, 3);
+      gprev = gam;
+      aprev = al;
+    }
+    if (owner) {
+#pragma unroll
+      for (int c = 0; c < 3; ++c) P.x[3 * node + c] = xr[c];
+    }
+    if (blockIdx.x == 0 && t == 0) {
+      P.st->origin = c0 + (unsigned long long)epoch * nb;
+      P.st->seq = seq + 1u;
+    }
+    return;
+  }
+
+  // x = 0; r = b; z = dinv*r; p = z; rz = r.z
+  double xr[3] = {0.0, 0.0, 0.0}, rr[3] = {0.0, 0.0, 0.0}, dv[3] = {0.0, 0.0, 0.0};
+  double pown[3] = {0.0, 0.0, 0.0}, qown[3] = {0.0, 0.0, 0.0};
+  double loc = 0.0;
+  if (owner) {
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      rr[c] = P.b[3 * node + c];
+      dv[c] = P.dinv[3 * node + c];
+      const double zv = dv[c] * rr[c];
+      ll_store(P.zll + c * nn + node, zv, fbase);
+      loc = fma(rr[c], zv, loc);
+    }
+  }
+  unsigned epoch = 0;
+  ++epoch;
+  double rz = br_allreduce(loc, P, fbase | epoch, c0 + epoch * nb, red, &tot);
+  double beta = 0.0;
+  for (int s = 0; s < P.steps; ++s) {
+    if (P.trace && s == 10) stamp(P.trace, 0);
+    // p = z + beta p on the brick + halo (z of step s carries flag fbase + s)
+    fill(fbase + unsigned(s), s > 0, beta);
+    __syncthreads();
+    if (P.trace && s == 10) stamp(P.trace, 5);
+    double av[3];
+    spmv(av);
     loc = 0.0;
     if (owner) {
-      const double av[3] = {a0 + rowpart[0][0][ln] + rowpart[1][0][ln],
-                            a1 + rowpart[0][1][ln] + rowpart[1][1][ln],
-                            a2 + rowpart[0][2][ln] + rowpart[1][2][ln]};
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
         pown[c] = pw[c * kBrWinMax + wctr];
@@ -570,12 +722,13 @@ void Pcg80::setup(const Grid& g, const double* A, const double* diag, double eps
     smem_bytes = int(sizeof(double)) * (kBrSmemA + 3 * kBrWinMax);
     SG_REQUIRE(smem_bytes <= smem_optin, "pcg80 brick kernel shared memory");
     SG_REQUIRE(2 * steps_ + 1 < 1024, "pcg80 step count too large for the packet flags");
-    SG_CUDA(cudaFuncSetAttribute(pcg80_brick_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 smem_bytes));
-    SG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pcg80_brick_kernel, kBrThreads,
-                                                          smem_bytes));
+    cgcg = getenv("SG_PCG80_CG") != nullptr;  // measured slower today (see DESIGN)
+    for (void* fn : {(void*)pcg80_brick_kernel<true>, (void*)pcg80_brick_kernel<false>})
+      SG_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes));
+    SG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+        &per_sm, cgcg ? pcg80_brick_kernel<true> : pcg80_brick_kernel<false>, kBrThreads, smem_bytes));
     SG_REQUIRE(per_sm >= 1, "pcg80 brick kernel cannot be resident");
-    slots.alloc(size_t(2 * nblocks));
+    slots.alloc(size_t(4 * nblocks));
     slots.zero(s);
     zll.alloc(size_t(3 * g.d.nnodes()));
     zll.zero(s);
@@ -621,7 +774,8 @@ void Pcg80::solve(const double* b, double* x, cudaStream_t s) {
     a.sz = sz;
     a.trace = trace;
     void* args[] = {&a};
-    SG_CUDA(cudaLaunchCooperativeKernel((void*)pcg80_brick_kernel, dim3(nblocks), dim3(kBrThreads),
+    void* fn = cgcg ? (void*)pcg80_brick_kernel<true> : (void*)pcg80_brick_kernel<false>;
+    SG_CUDA(cudaLaunchCooperativeKernel(fn, dim3(nblocks), dim3(kBrThreads),
                                         args, size_t(smem_bytes), s));
     SG_CHECK_LAUNCH();
     return;

@@ -19,8 +19,8 @@ for rep in range(3):
     t = t[t[:, 0] > 0]
     t0 = t[:, 0].min()
     rel = (t - t0) / 1e3
-    # stamps: 0 step start, 1 phase A done, 2 pq known, 3 phase B done, 4 rzn known
-    for k, name in enumerate(["start", "A_done", "pq_out", "B_done", "rz_out", "redA_issued", "spinA_exit", "redA_end"]):
+    # stamps (brick kernel): 0 step start, 5 window staged, 1 phase A done, 2 pq known, 3 phase B done, 4 rzn known
+    for k, name in enumerate(["start", "A_done", "pq_out", "B_done", "rz_out", "fill_done", "s6", "s7"]):
         col = rel[:, k]
         print(f"{name:7s} min {col.min():6.2f} med {np.median(col):6.2f} max {col.max():6.2f} us "
               f"(argmax blk {int(col.argmax())})")
