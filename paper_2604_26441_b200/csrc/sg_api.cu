@@ -89,6 +89,13 @@ int sg_fine_create(int nx, int ny, int nz, const uint8_t* dof_mask, const double
     }
     for (int q = 0; q < 24; ++q) f->op.kdiag.d[q] = ke[q * 24 + q];
     f->op.walsh_ok = sg::walsh_params(ke, f->op.kw64, f->op.kw32);
+    if (sg::p32_supported(f->op)) {  // P32 staging of the node-layout FP32 apply
+      const size_t n32 = size_t(sg::p32_size(f->op.grid.d));
+      f->op.p32a.alloc(n32);
+      f->op.p32b.alloc(n32);
+      f->op.p32a.zero(s);
+      f->op.p32b.zero(s);
+    }
     const size_t nd = size_t(3 * f->op.grid.d.nnodes());
     f->w.u64.alloc(nd);
     f->w.y64.alloc(nd);
@@ -691,6 +698,9 @@ extern "C" int sg_hier_profile(sg_hier* h, int what, int reps, double* ms_avg, v
     const int64_t nd0 = L0.nd();
     sg::DBuf<double> a(static_cast<size_t>(nd0)), b(static_cast<size_t>(nd0));
     sg::DBuf<float> fa(static_cast<size_t>(nd0)), fb(static_cast<size_t>(nd0));
+    const size_t n32 = size_t(sg::p32_size(H.fine->grid.d));
+    sg::DBuf<float> pa(n32), pb(n32);
+    pa.zero(s);
     sg::DBuf<uint8_t> flush(size_t(256) << 20);
     SG_CUDA(cudaMemsetAsync(a.p, 0, sizeof(double) * nd0, s));
     SG_CUDA(cudaMemsetAsync(fa.p, 0, sizeof(float) * nd0, s));
@@ -702,7 +712,10 @@ extern "C" int sg_hier_profile(sg_hier* h, int what, int reps, double* ms_avg, v
       SG_CUDA(cudaMemsetAsync(flush.p, r & 0xff, flush.n, s));
       SG_CUDA(cudaEventRecord(e0, s));
       switch (what) {
-        case 0: sg::fine_apply_f32(*H.fine, fa.p, fb.p, s); break;
+        case 0:  // the level-0 FP32 apply the V-cycle runs (P32 layout when supported)
+          if (sg::p32_supported(*H.fine)) sg::fine_apply_p32(*H.fine, pa.p, pb.p, s);
+          else sg::fine_apply_f32(*H.fine, fa.p, fb.p, s);
+          break;
         case 1: sg::fine_apply_f64(*H.fine, a.p, b.p, s); break;
         case 2: {
           SG_REQUIRE(H.lv.size() > 1, "no level 1");

@@ -112,7 +112,18 @@ void fine_apply_f64(const FineOp& op, const double* u, double* y, cudaStream_t s
   if (op.walsh_ok) fine_apply_walsh_f64(op, u, y, s);
   else fine_apply_dense_f64(op, u, y, s);
 }
+// FP32 on node-layout vectors: converted through the P32 layout and the
+// packed FP32x2 kernel (sg_fine_pk.cu); SG_FINE_WALSH1=1 selects the scalar
+// one-element-per-thread Walsh kernel (comparison runs).
 void fine_apply_f32(const FineOp& op, const float* u, float* y, cudaStream_t s) {
+  static const bool scalar = getenv("SG_FINE_WALSH1") != nullptr;
+  if (!scalar && op.p32a.n >= size_t(p32_size(op.grid.d)) && p32_supported(op)) {
+    FineOp& m = const_cast<FineOp&>(op);
+    to_p32<float>(op.grid.d, u, m.p32a.p, s);
+    fine_apply_p32(op, m.p32a.p, m.p32b.p, s);
+    from_p32<float>(op.grid.d, m.p32b.p, y, s);
+    return;
+  }
   if (op.walsh_ok) fine_apply_walsh_f32(op, u, y, s);
   else fine_apply_dense_f32(op, u, y, s);
 }

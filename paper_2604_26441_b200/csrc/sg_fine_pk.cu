@@ -1,0 +1,471 @@
+// Level-0 matrix-free FP32 apply on packed FP32x2 arithmetic (FADD2 / FMUL2 /
+// FFMA2, sm_100a).  fine_operator.py:56-77 (FP32 tag): y = K_ff u with the
+// element modulus applied per element.
+//
+// Same algebra as sg_fine_walsh.cu (tensor Walsh basis, 45-entry Kw, SURVEY
+// A.6) but re-tiled so that every FP32 instruction does two elements' work:
+//  * a thread owns an x-PAIR of elements (e0, e1) = (ex, ex+1) of one element
+//    row and streams the pair up a z-chunk; every Walsh, scaling, Kw and
+//    inverse step runs on float2 lanes (e0, e1) -> half the FP32 issue slots;
+//  * the separable transform is shared: the x/y stage of a node plane is
+//    computed once and reused by the layer below and the layer above (in
+//    registers); the inverse adds the two layers sharing a node plane in the
+//    Walsh-xy domain before the xy inverse (12 adds instead of 24);
+//  * a CTA = R element rows x P pairs, flattened (t = row*P + pair), so the
+//    tile fits any nx (P = (nx+2)/2 pairs covers a whole row for nx <= 100 with
+//    two phantom columns); neighbour partial sums go through shared memory
+//    (one barrier per layer, double-buffered) in a fixed order, so every
+//    output is bit-reproducible run to run;
+//  * ownership: pair p owns node columns ex+1 and ex+2 (the last pair only
+//    ex+1), local row r < R-1 owns node row ej+1; tiles overlap by one element
+//    column / row / layer (recomputed halo, no atomics).
+#include <cmath>
+#include "sg_kernels.cuh"
+
+namespace sg {
+
+
+constexpr int kPkMaxThreads = 512;
+
+__device__ __forceinline__ float2 add2(float2 a, float2 b) { return __fadd2_rn(a, b); }
+__device__ __forceinline__ float2 sub2(float2 a, float2 b) {
+  return __fadd2_rn(a, make_float2(-b.x, -b.y));
+}
+__device__ __forceinline__ float2 mul2(float2 a, float2 b) { return __fmul2_rn(a, b); }
+__device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) { return __ffma2_rn(a, b, c); }
+// x/y stage of one node plane for an element pair: raw[y][x][c] (x = node
+// columns ex, ex+1, ex+2; y = rows ej, ej+1) -> Q[c][m], m = mode in the xy
+// Walsh basis (0: const, 1: x, 2: y, 3: xy), lanes = (e0, e1).
+__device__ __forceinline__ void plane_xy(const float (&raw)[2][3][3], float2 (&Q)[3][4]) {
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    float2 S[2], D[2];
+#pragma unroll
+    for (int y = 0; y < 2; ++y) {
+      const float2 A = make_float2(raw[y][0][c], raw[y][1][c]);  // x = 0 corners
+      const float2 B = make_float2(raw[y][1][c], raw[y][2][c]);  // x = 1 corners
+      S[y] = add2(A, B);
+      D[y] = sub2(A, B);
+    }
+    Q[c][0] = add2(S[0], S[1]);
+    Q[c][2] = sub2(S[0], S[1]);
+    Q[c][1] = add2(D[0], D[1]);
+    Q[c][3] = sub2(D[0], D[1]);
+  }
+}
+
+// Block structure of Kw/64 (verified on the host by pk_params): with index
+// 3*mode + comp the 45 nonzeros form
+//   {3,7,14} and {11,16,18}: [[p,q,q],[q,p,q],[q,q,p]]  -> (p-q) v_i + q * sum
+//   {4,6}, {5,12}, {8,13}:     [[c,c],[c,c]]            -> c * (v_i + v_j), both rows
+//   {9,20}, {10,17}, {15,19}:  [[d,e],[e,d]]
+//   {21}, {22}, {23}:          h
+// so w = Kw (E v) costs 33 packed ops plus 8 per-element coefficient scalings
+// (E folded into the coefficients) instead of 21 + 45.
+struct PkCoef {
+  float amb, b, c, d, e, fmg, g, h;
+};
+
+// Level-0 FP32 vectors in the "P32" layout: component-planar rows,
+//   index(c, i, j, k) = ((k*NY + j)*3 + c)*XS + i,  XS = NX rounded up to even,
+// padding (i >= NX) held at 0.  A pair's two x-nodes are one aligned 8-byte
+// load/store and a warp's lanes touch contiguous 256 B: the node layout's
+// 12-byte node stride made every scalar access span six 128-byte lines.
+enum PkMode : int { PK_Y = 0, PK_CHEB = 1, PK_RES = 2 };
+
+// Fused epilogues (smoothers.py:90-110 / hierarchy.py:214 rounding points,
+// FP32 ops per lane, no contraction):
+//  PK_CHEB: r = b - Kx; d' = A*(dinv*r) + AC*d (first: d' = A*(dinv*r));
+//           x' = x + d'   (x' into a different buffer: neighbours still read x)
+//  PK_RES:  out64 = r64 - f64(Kx)   (node layout FP64, the coarse-level residual)
+struct PkEpi {
+  const float* b = nullptr;
+  const float* dinv = nullptr;
+  float* d = nullptr;
+  float* xout = nullptr;
+  float A = 0.f, AC = 0.f;
+  int first = 0;
+  const double* r64 = nullptr;
+  double* out64 = nullptr;
+};
+
+// Prefetch loads as volatile asm: issued where written (the compiler may not
+// sink them next to their use to save registers, which exposed the latency).
+__device__ __forceinline__ float ldp(const float* p) {
+  float v;
+  asm volatile("ld.global.nc.f32 %0, [%1];" : "=f"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ float2 ldp2(const float* p) {
+  float2 v;
+  asm volatile("ld.global.nc.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "l"(p));
+  return v;
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(kPkMaxThreads, 1)
+fine_pk_kernel(GridDesc g, const uint8_t* __restrict__ nmask, const float* __restrict__ u,
+               float* __restrict__ yout, const float* __restrict__ E, PkCoef C, int P, int R,
+               int kchunk, int XS, PkEpi ep) {
+  // published partials [buf][q][thread]: q 0..2 = i0(row 0), 3..5 = i1(row 0),
+  // 6..8 = i2(row 0), 9..11 = i2(row 1), 3 comps each
+  __shared__ float pub[2][12][kPkMaxThreads];
+  const int t = threadIdx.x, lane = t & 31;
+  const int row = t / P, pair = t - row * P;
+  const bool live = row < R;
+  const int NX = g.nx + 1, NY = g.ny + 1;
+  const int ex = 2 * pair;  // e0; nodes ex, ex+1, ex+2
+  const int ej = int(blockIdx.y) * (R - 1) - 1 + row;
+  const int k0 = int(blockIdx.z) * kchunk;
+  const int k1 = min(k0 + kchunk, g.nz + 1);  // output node planes [k0, k1)
+  const int64_t pl = int64_t(3) * XS * NY;    // one node plane in P32
+  // i2 comes from lane+1's first node unless lane+1 is another row / warp
+  const bool fix = lane == 31 || pair == P - 1 || !live;
+  // row pointers (rows ej, ej+1, clamped), one node plane per layer
+  const float* up[2];
+  {
+    const int pk = min(max(k0 - 1, 0), g.nz);
+#pragma unroll
+    for (int y = 0; y < 2; ++y)
+      up[y] = u + int64_t(pk) * pl + int64_t(3) * XS * min(max(ej + y, 0), g.ny) + ex;
+  }
+  const bool rowin = live && ej >= 0 && ej < g.ny;
+  const float m0 = (rowin && ex < g.nx) ? 1.f : 0.f;
+  const float m1 = (rowin && ex + 1 < g.nx) ? 1.f : 0.f;
+  const int64_t estride = int64_t(g.nx) * g.ny;
+  const int64_t erow = int64_t(g.nx) * min(max(ej, 0), g.ny - 1);
+  const float* Ep0 = E + erow + min(ex, g.nx - 1);
+  const float* Ep1 = E + erow + min(ex + 1, g.nx - 1);
+
+  // ownership: nodes (ex, ex+1) of node row ej+1
+  const int on = ej + 1;
+  const bool own = live && row < R - 1 && on >= 0 && on <= g.ny && ex <= g.nx;
+  const bool own1 = ex + 1 <= g.nx;
+  const int64_t orow = int64_t(3) * XS * max(on, 0) + ex + int64_t(k0) * pl;  // + c*XS
+  const int64_t onode = int64_t(ex) + int64_t(NX) * max(on, 0) + int64_t(k0) * NX * NY;
+
+  float2 Qlo[3][4], Qhi[3][4], carry[3][4];
+  float2 A[2][3];
+  float a2[2][3];
+  auto load_plane = [&]() {
+#pragma unroll
+    for (int y = 0; y < 2; ++y)
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        A[y][c] = ldp2(up[y] + c * XS);
+        a2[y][c] = ldp(up[y] + c * XS + (fix ? 2 : 0));
+      }
+  };
+  auto plane_q = [&](float2 (&Q)[3][4]) {
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      float2 S[2], D[2];
+#pragma unroll
+      for (int y = 0; y < 2; ++y) {
+        const float nb = __shfl_down_sync(0xffffffffu, A[y][c].x, 1);
+        const float2 B = make_float2(A[y][c].y, fix ? a2[y][c] : nb);
+        S[y] = add2(A[y][c], B);
+        D[y] = sub2(A[y][c], B);
+      }
+      Q[c][0] = add2(S[0], S[1]);
+      Q[c][2] = sub2(S[0], S[1]);
+      Q[c][1] = add2(D[0], D[1]);
+      Q[c][3] = sub2(D[0], D[1]);
+    }
+  };
+  auto advance = [&](bool more) {
+    if (more) {
+      up[0] += pl;
+      up[1] += pl;
+    }
+  };
+  int pk = k0 - 1;
+  load_plane();
+  plane_q(Qlo);
+  advance(pk >= 0 && pk < g.nz);
+  ++pk;
+  load_plane();  // plane k0
+#pragma unroll
+  for (int c = 0; c < 3; ++c)
+#pragma unroll
+    for (int m = 0; m < 4; ++m) carry[c][m] = make_float2(0.f, 0.f);
+  int buf = 0;
+  int64_t oplane = 0;  // output planes written so far
+  // element moduli, prefetched one layer ahead (0 outside the domain)
+  // raw moduli of layer ek (the domain mask is applied when they are used)
+  auto load_E = [&](int ek) {
+    const int64_t eo = int64_t(min(max(ek, 0), g.nz - 1)) * estride;
+    return make_float2(ldp(Ep0 + eo), ldp(Ep1 + eo));
+  };
+  float2 Eraw = load_E(k0 - 1);
+
+  for (int ek = k0 - 1; ek < k1; ++ek) {
+    plane_q(Qhi);  // node plane ek+1
+    advance(pk >= 0 && pk < g.nz);
+    ++pk;
+    load_plane();  // prefetch node plane ek+2
+    const float2 En = load_E(ek + 1);
+    const bool kin = ek >= 0 && ek < g.nz;
+    const float2 Es = mul2(Eraw, make_float2(kin ? m0 : 0.f, kin ? m1 : 0.f));
+    const float2 kA = mul2(Es, make_float2(C.amb, C.amb)), kB = mul2(Es, make_float2(C.b, C.b));
+    const float2 kC = mul2(Es, make_float2(C.c, C.c)), kD = mul2(Es, make_float2(C.d, C.d));
+    const float2 kE = mul2(Es, make_float2(C.e, C.e)), kF = mul2(Es, make_float2(C.fmg, C.fmg));
+    const float2 kG = mul2(Es, make_float2(C.g, C.g)), kH = mul2(Es, make_float2(C.h, C.h));
+    // z stage -> v[3*mode + c], modes 1..7
+    float2 v[24];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+#pragma unroll
+      for (int m = 1; m < 4; ++m) v[3 * m + c] = add2(Qlo[c][m], Qhi[c][m]);
+#pragma unroll
+      for (int m = 0; m < 4; ++m) v[3 * (m + 4) + c] = sub2(Qlo[c][m], Qhi[c][m]);
+    }
+    // w = (E Kw) v, block form
+    float2 w[24];
+    {
+      const float2 t1 = mul2(kB, add2(add2(v[3], v[7]), v[14]));
+      w[3] = fma2(kA, v[3], t1);
+      w[7] = fma2(kA, v[7], t1);
+      w[14] = fma2(kA, v[14], t1);
+      w[4] = w[6] = mul2(kC, add2(v[4], v[6]));
+      w[5] = w[12] = mul2(kC, add2(v[5], v[12]));
+      w[8] = w[13] = mul2(kC, add2(v[8], v[13]));
+      w[9] = fma2(kD, v[9], mul2(kE, v[20]));
+      w[20] = fma2(kD, v[20], mul2(kE, v[9]));
+      w[10] = fma2(kD, v[10], mul2(kE, v[17]));
+      w[17] = fma2(kD, v[17], mul2(kE, v[10]));
+      w[15] = fma2(kD, v[15], mul2(kE, v[19]));
+      w[19] = fma2(kD, v[19], mul2(kE, v[15]));
+      const float2 t2 = mul2(kG, add2(add2(v[11], v[16]), v[18]));
+      w[11] = fma2(kF, v[11], t2);
+      w[16] = fma2(kF, v[16], t2);
+      w[18] = fma2(kF, v[18], t2);
+      w[21] = mul2(kH, v[21]);
+      w[22] = mul2(kH, v[22]);
+      w[23] = mul2(kH, v[23]);
+    }
+    // inverse z stage + the layer below's top half (same node plane ek)
+    float2 T[3][4];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      T[c][0] = add2(carry[c][0], w[12 + c]);
+      carry[c][0] = make_float2(-w[12 + c].x, -w[12 + c].y);
+#pragma unroll
+      for (int m = 1; m < 4; ++m) {
+        T[c][m] = add2(carry[c][m], add2(w[3 * m + c], w[3 * (m + 4) + c]));
+        carry[c][m] = sub2(w[3 * m + c], w[3 * (m + 4) + c]);
+      }
+    }
+    if (ek >= k0) {
+      // xy inverse -> corner partials of this pair on plane ek
+      float n0[2][3], n1[2][3], n2[2][3];
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        const float2 S0 = add2(T[c][0], T[c][2]), D0 = add2(T[c][1], T[c][3]);
+        const float2 S1 = sub2(T[c][0], T[c][2]), D1 = sub2(T[c][1], T[c][3]);
+        const float2 r0x0 = add2(S0, D0), r0x1 = sub2(S0, D0);
+        const float2 r1x0 = add2(S1, D1), r1x1 = sub2(S1, D1);
+        n0[0][c] = r0x0.x;
+        n1[0][c] = r0x1.x + r0x0.y;
+        n2[0][c] = r0x1.y;
+        n0[1][c] = r1x0.x;
+        n1[1][c] = r1x1.x + r1x0.y;
+        n2[1][c] = r1x1.y;
+      }
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        pub[buf][c][t] = n0[0][c];
+        pub[buf][3 + c][t] = n1[0][c];
+        pub[buf][6 + c][t] = n2[0][c];
+        pub[buf][9 + c][t] = n2[1][c];
+      }
+      __syncthreads();
+      if (own) {
+        const bool left = pair > 0;
+        const int64_t nodei = onode + oplane * int64_t(NX) * NY;
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          // node ex: (own e0 + left pair's e1) + (same, row above)
+          float y0 = n0[1][c] + (left ? pub[buf][9 + c][t - 1] : 0.f);
+          y0 = y0 + (pub[buf][c][t + P] + (left ? pub[buf][6 + c][t + P - 1] : 0.f));
+          // node ex+1: own pair + the row above's pair
+          float y1 = n1[1][c] + pub[buf][3 + c][t + P];
+          const bool f0 = g.xface ? ex == 0 : ((nmask[nodei] >> c) & 1);
+          const bool f1 = !own1 || (g.xface ? false : ((nmask[nodei + 1] >> c) & 1));
+          y0 = f0 ? 0.f : y0;
+          y1 = f1 ? 0.f : y1;
+          const int64_t o = orow + oplane * pl + int64_t(c) * XS;
+          if constexpr (MODE == PK_Y) {
+            *reinterpret_cast<float2*>(yout + o) = make_float2(y0, y1);
+          } else if constexpr (MODE == PK_CHEB) {
+            const float2 bb = *reinterpret_cast<const float2*>(ep.b + o);
+            const float2 di = *reinterpret_cast<const float2*>(ep.dinv + o);
+            const float2 xx = *reinterpret_cast<const float2*>(u + o);
+            // scalar round-to-nearest intrinsics: never contracted (ptxas
+            // was seen fusing even explicit mul.rn/add.rn .f32x2 into FFMA2)
+            float2 dn = make_float2(__fmul_rn(ep.A, __fmul_rn(di.x, __fsub_rn(bb.x, y0))),
+                                    __fmul_rn(ep.A, __fmul_rn(di.y, __fsub_rn(bb.y, y1))));
+            if (!ep.first) {
+              const float2 dd = *reinterpret_cast<const float2*>(ep.d + o);
+              dn.x = __fadd_rn(dn.x, __fmul_rn(ep.AC, dd.x));
+              dn.y = __fadd_rn(dn.y, __fmul_rn(ep.AC, dd.y));
+            }
+            *reinterpret_cast<float2*>(ep.d + o) = dn;
+            *reinterpret_cast<float2*>(ep.xout + o) = make_float2(__fadd_rn(xx.x, dn.x), __fadd_rn(xx.y, dn.y));
+          } else {
+            const int64_t q = 3 * nodei + c;
+            ep.out64[q] = __dsub_rn(ep.r64[q], double(y0));
+            if (own1) ep.out64[q + 3] = __dsub_rn(ep.r64[q + 3], double(y1));
+          }
+        }
+      }
+      ++oplane;
+      buf ^= 1;
+    }
+#pragma unroll
+    for (int c = 0; c < 3; ++c)
+#pragma unroll
+      for (int m = 0; m < 4; ++m) Qlo[c][m] = Qhi[c][m];
+    Eraw = En;
+  }
+}
+
+// Block parameters of Kw/64 (fp32); false when Ke does not have the block
+// structure (the scalar Walsh kernel is used instead).
+static bool pk_params(const FineOp& op, PkCoef& C) {
+  double Kw[24][24] = {};
+  for (int q = 0; q < 45; ++q) Kw[kKwRowHost(q)][kKwColHost(q)] = op.kw64.v[q];
+  const double a = Kw[3][3], b = Kw[3][7], c = Kw[4][4], d = Kw[9][9], e = Kw[9][20],
+               f = Kw[11][11], gg = Kw[11][16], h = Kw[21][21];
+  double want[24][24] = {};
+  auto blk3 = [&](int i, int j, int k, double p, double q) {
+    const int id[3] = {i, j, k};
+    for (int r = 0; r < 3; ++r)
+      for (int s = 0; s < 3; ++s) want[id[r]][id[s]] = r == s ? p : q;
+  };
+  auto blk2 = [&](int i, int j, double p, double q) {
+    want[i][i] = want[j][j] = p;
+    want[i][j] = want[j][i] = q;
+  };
+  blk3(3, 7, 14, a, b);
+  blk3(11, 16, 18, f, gg);
+  blk2(4, 6, c, c);
+  blk2(5, 12, c, c);
+  blk2(8, 13, c, c);
+  blk2(9, 20, d, e);
+  blk2(10, 17, d, e);
+  blk2(15, 19, d, e);
+  want[21][21] = want[22][22] = want[23][23] = h;
+  double mx = 0.0;
+  for (int r = 0; r < 24; ++r)
+    for (int s = 0; s < 24; ++s) mx = std::max(mx, std::fabs(Kw[r][s]));
+  for (int r = 0; r < 24; ++r)
+    for (int s = 0; s < 24; ++s)
+      if (std::fabs(Kw[r][s] - want[r][s]) > 1e-12 * mx) return false;
+  C.amb = float(a - b);
+  C.b = float(b);
+  C.c = float(c);
+  C.d = float(d);
+  C.e = float(e);
+  C.fmg = float(f - gg);
+  C.g = float(gg);
+  C.h = float(h);
+  return true;
+}
+
+int p32_xs(const GridDesc& g) { return ((g.nx + 1) + 1) & ~1; }
+int64_t p32_size(const GridDesc& g) {
+  return int64_t(3) * p32_xs(g) * (g.ny + 1) * (g.nz + 1) + 4;  // + slack for the i2 reads
+}
+
+bool p32_supported(const FineOp& op) {
+  PkCoef C;
+  return op.walsh_ok && op.grid.d.nx + 1 <= 2 * 64 && pk_params(op, C);
+}
+
+template <int MODE>
+static void launch_pk(const FineOp& op, const float* u, float* y, const PkEpi& ep, cudaStream_t s) {
+  PkCoef C;
+  SG_REQUIRE(op.walsh_ok && pk_params(op, C), "P32 apply: element matrix lacks the Walsh block form");
+  const GridDesc& g = op.grid.d;
+  const int P = (g.nx + 2) / 2;  // pairs covering nodes 0..nx (a phantom element if nx is odd)
+  SG_REQUIRE(P <= 64, "P32 apply: nx too large for a whole-row tile");
+  int R = std::max(2, kPkMaxThreads / P);
+  R = std::min(R, g.ny + 2);
+  const int tilesy = (g.ny + 1 + (R - 1) - 1) / (R - 1);
+  const int planes = g.nz + 1;
+  // z chunks: fill the SMs once (one CTA per SM), each chunk pays one halo layer
+  int nch = std::max(1, std::min(planes, kNumSMs / std::max(1, tilesy)));
+  const int kchunk = (planes + nch - 1) / nch;
+  nch = (planes + kchunk - 1) / kchunk;
+  const int threads = ((P * R + 31) / 32) * 32;
+  dim3 grid(1, tilesy, nch);
+  fine_pk_kernel<MODE><<<grid, threads, 0, s>>>(g, op.grid.nmask.p, u, y, op.E32.p, C, P, R, kchunk,
+                                                p32_xs(g), ep);
+  SG_CHECK_LAUNCH();
+}
+
+void fine_apply_p32(const FineOp& op, const float* u, float* y, cudaStream_t s) {
+  launch_pk<PK_Y>(op, u, y, PkEpi{}, s);
+}
+void fine_apply_p32_cheb(const FineOp& op, const float* x, float* xout, const float* b,
+                         const float* dinv, float* d, float A, float AC, bool first, cudaStream_t s) {
+  PkEpi ep;
+  ep.b = b;
+  ep.dinv = dinv;
+  ep.d = d;
+  ep.xout = xout;
+  ep.A = A;
+  ep.AC = AC;
+  ep.first = first ? 1 : 0;
+  launch_pk<PK_CHEB>(op, x, nullptr, ep, s);
+}
+void fine_apply_p32_res(const FineOp& op, const float* x, const double* r64, double* out64,
+                        cudaStream_t s) {
+  PkEpi ep;
+  ep.r64 = r64;
+  ep.out64 = out64;
+  launch_pk<PK_RES>(op, x, nullptr, ep, s);
+}
+
+// ------------------------------------------------ P32 <-> node conversions
+template <class Tin>
+__global__ void to_p32_kernel(GridDesc g, int XS, const Tin* __restrict__ src, float* __restrict__ dst,
+                              int64_t n) {
+  const int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (q >= n) return;
+  const int i = int(q % XS);
+  const int64_t rc = q / XS;  // (k*NY + j)*3 + c
+  const int c = int(rc % 3);
+  const int64_t node = (rc / 3) * (g.nx + 1) + i;
+  dst[q] = i <= g.nx ? float(src[3 * node + c]) : 0.f;
+}
+template <class Tout>
+__global__ void from_p32_kernel(GridDesc g, int XS, const float* __restrict__ src, Tout* __restrict__ dst,
+                                int64_t nd) {
+  const int64_t d = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (d >= nd) return;
+  const int c = int(d % 3);
+  const int64_t node = d / 3;
+  const int i = int(node % (g.nx + 1));
+  const int64_t jk = node / (g.nx + 1);
+  dst[d] = Tout(src[(jk * 3 + c) * XS + i]);
+}
+template <class Tin>
+void to_p32(const GridDesc& g, const Tin* src, float* dst, cudaStream_t s) {
+  const int64_t n = int64_t(3) * p32_xs(g) * (g.ny + 1) * (g.nz + 1);
+  to_p32_kernel<Tin><<<grid_blocks(n, 256), 256, 0, s>>>(g, p32_xs(g), src, dst, n);
+  SG_CHECK_LAUNCH();
+}
+template <class Tout>
+void from_p32(const GridDesc& g, const float* src, Tout* dst, cudaStream_t s) {
+  const int64_t nd = 3 * g.nnodes();
+  from_p32_kernel<Tout><<<grid_blocks(nd, 256), 256, 0, s>>>(g, p32_xs(g), src, dst, nd);
+  SG_CHECK_LAUNCH();
+}
+template void to_p32<double>(const GridDesc&, const double*, float*, cudaStream_t);
+template void to_p32<float>(const GridDesc&, const float*, float*, cudaStream_t);
+template void from_p32<double>(const GridDesc&, const float*, double*, cudaStream_t);
+template void from_p32<float>(const GridDesc&, const float*, float*, cudaStream_t);
+
+}  // namespace sg

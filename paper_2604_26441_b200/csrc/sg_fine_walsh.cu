@@ -32,6 +32,9 @@ const int kKwColH[45] = {3, 7, 14, 4, 6, 5, 12, 4, 6, 3, 7, 14, 8, 13, 9,
                          20, 10, 17, 11, 16, 18, 5, 12, 8, 13, 3, 7, 14, 15, 19,
                          11, 16, 18, 10, 17, 11, 16, 18, 15, 19, 9, 20, 21, 22, 23};
 
+int kKwRowHost(int q) { return kKwRowH[q]; }
+int kKwColHost(int q) { return kKwColH[q]; }
+
 bool walsh_params(const double* ke, KwParam<double>& p64, KwParam<float>& p32) {
   double Kw[24][24];
   double maxabs = 0.0;

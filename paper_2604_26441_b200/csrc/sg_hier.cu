@@ -200,8 +200,80 @@ static void smooth_t(Hier& H, Level& L, const T* b, const double* x0, double* ou
   }
 }
 
+// Level-0 FP32 smoother on P32 vectors: every step after the first is ONE
+// kernel (apply + residual + Chebyshev/Jacobi update, fine_apply_p32_cheb),
+// the x iterate ping-pongs between x32 and x32b.  Same FP32 rounding points
+// as smooth_t (smoothers.py:90-131).
+static void smooth_p32(Hier& H, Level& L, const double* b64, const double* x0, double* out,
+                       cudaStream_t s) {
+  const FineOp& op = *H.fine;
+  const GridDesc& g = L.g->d;
+  const int64_t n = L.n32();
+  float* x = L.w.x32.p;
+  float* xb = L.w.x32b.p;
+  float* d = L.w.dd32.p;
+  float* b = L.w.b32.p;
+  const float* dinv = L.dinv32p.p;
+  to_p32<double>(g, b64, b, s);
+  static const bool unfused = std::getenv("SG_P32_UNFUSED") != nullptr;  // A/B check
+  int done = 0;
+  if (L.kind == 0) {  // Chebyshev
+    const double lam = L.lam;
+    const double sigma = 0.5 * (lam + L.alpha * lam);
+    const double delta = 0.5 * (lam - L.alpha * lam);
+    const float c0 = float(1.0 / sigma);
+    if (!x0) {
+      launch_ew(n, s, [&](int nb, int nt) { cheb_first0_kernel<float><<<nb, nt, 0, s>>>(n, dinv, b, c0, d, x); });
+    } else {
+      to_p32<double>(g, x0, x, s);
+      if (unfused) {
+        fine_apply_p32(op, x, L.w.y32.p, s);
+        launch_ew(n, s, [&](int nb, int nt) { cheb_first_kernel<float><<<nb, nt, 0, s>>>(n, dinv, b, L.w.y32.p, c0, d, x); });
+      } else {
+        fine_apply_p32_cheb(op, x, xb, b, dinv, d, c0, 0.f, true, s);
+        std::swap(x, xb);
+      }
+    }
+    double a = 2.0 / sigma;
+    for (int it = 1; it < L.degree; ++it) {
+      const double c = delta * delta * a / 4.0;
+      a = 1.0 / (sigma - c);
+      if (unfused) {
+        fine_apply_p32(op, x, L.w.y32.p, s);
+        const float A = float(a), AC = float(a * c);
+        launch_ew(n, s, [&](int nb, int nt) { cheb_step_kernel<float><<<nb, nt, 0, s>>>(n, dinv, b, L.w.y32.p, A, AC, d, x); });
+      } else {
+        fine_apply_p32_cheb(op, x, xb, b, dinv, d, float(a), float(a * c), false, s);
+        std::swap(x, xb);
+      }
+    }
+    done = 1;
+  } else {  // damped Jacobi: x = x + w*(dinv*(b - Kx))
+    const float w = float(L.omega);
+    int steps = L.degree;
+    if (!x0) {
+      launch_ew(n, s, [&](int nb, int nt) { jac_first0_kernel<float><<<nb, nt, 0, s>>>(n, dinv, b, w, x); });
+      steps -= 1;
+    } else {
+      to_p32<double>(g, x0, x, s);
+    }
+    for (int it = 0; it < steps; ++it) {
+      fine_apply_p32(op, x, L.w.y32.p, s);
+      launch_ew(n, s, [&](int nb, int nt) { jac_step_kernel<float><<<nb, nt, 0, s>>>(n, dinv, b, L.w.y32.p, w, x); });
+    }
+    done = 1;
+  }
+  (void)done;
+  L.w.xcur = x;
+  from_p32<double>(g, x, out, s);
+}
+
 void level_smooth(Hier& H, int l, const double* b, const double* x0, double* out, cudaStream_t s) {
   Level& L = *H.lv[size_t(l)];
+  if (L.p32) {
+    smooth_p32(H, L, b, x0, out, s);
+    return;
+  }
   if (L.tag == TAG_FP64) {
     smooth_t<double>(H, L, b, x0, out, s);
   } else {
@@ -231,6 +303,16 @@ void cycle(Hier& H, int l, int gamma, cudaStream_t s) {
     if (L.tag == TAG_FP64) {
       level_apply(H, L, TAG_FP64, x64, L.w.y64.p, s);
       launch_ew(n, s, [&](int nb, int nt) { residual_kernel<double><<<nb, nt, 0, s>>>(n, L.w.r.p, L.w.y64.p, L.w.x.p); });
+    } else if (L.p32) {
+      // x32 = f32(x64): the smoother's last FP32 iterate on the first pass
+      // (x64 = f64 of it, so the round trip is exact); re-converted after a
+      // coarse correction (W-cycle)
+      float* xc = L.w.xcur;
+      if (g > 0 || !xc) {
+        xc = L.w.x32.p;
+        to_p32<double>(L.g->d, x64, xc, s);
+      }
+      fine_apply_p32_res(*H.fine, xc, L.w.r.p, L.w.x.p, s);
     } else {
       cvt_f64_to_f32(n, x64, L.w.x32.p, s);
       level_apply(H, L, L.tag, L.w.x32.p, L.w.y32.p, s);
@@ -354,7 +436,7 @@ void fine_floored_diag(FineOp& op, FineWork& w, cudaStream_t s) {
   w.diag_ready = true;
 }
 
-static void alloc_work(Level& L) {
+static void alloc_work(Level& L, cudaStream_t s) {
   const size_t n = size_t(L.nd());
   L.w.r.alloc(n);
   L.w.x.alloc(n);
@@ -362,10 +444,16 @@ static void alloc_work(Level& L) {
   L.w.y64.alloc(n);
   L.w.dd64.alloc(n);
   if (L.tag != TAG_FP64) {
-    L.w.b32.alloc(n);
-    L.w.x32.alloc(n);
-    L.w.y32.alloc(n);
-    L.w.dd32.alloc(n);
+    const size_t n32 = L.p32 ? size_t(L.n32()) : n;
+    L.w.b32.alloc(n32);
+    L.w.x32.alloc(n32);
+    L.w.y32.alloc(n32);
+    L.w.dd32.alloc(n32);
+    if (L.p32) {
+      L.w.x32b.alloc(n32);
+      // padding entries must read 0 (they are never written)
+      for (auto* b : {&L.w.b32, &L.w.x32, &L.w.y32, &L.w.dd32, &L.w.x32b}) b->zero(s);
+    }
   }
 }
 
@@ -438,7 +526,13 @@ std::unique_ptr<Hier> hier_build(FineOp* fine, FineWork& fw, const HParams& p, c
       stencil_tile<double>(*L.g, L.st.A64.p, L.st.T64, s);
     }
     launch_ew(int64_t(n), s, [&](int nb, int nt) { recip_kernel<<<nb, nt, 0, s>>>(int64_t(n), L.diag.p, L.dinv.p, L.dinv32.p); });
-    alloc_work(L);
+    L.p32 = L.is_fine && L.tag == TAG_FP32 && p32_supported(*fine) && !std::getenv("SG_NO_P32");
+    if (L.p32) {  // dinv32 in the P32 layout (0 on padding); the node-layout
+                  // copy stays for the slab windows (dist_build)
+      L.dinv32p.alloc(size_t(L.n32()));
+      to_p32<float>(L.g->d, L.dinv32.p, L.dinv32p.p, s);
+    }
+    alloc_work(L, s);
     if (lam_cache && i < n_cache) {
       L.lam = lam_cache[i];
     } else {
@@ -569,6 +663,13 @@ std::unique_ptr<DistPart> dist_build(Hier& F, int n_dist, const int* planes, con
   wf.kw32 = ff.kw32;
   wf.walsh_ok = ff.walsh_ok;
   wf.emax = ff.emax;
+  if (p32_supported(wf)) {  // same FP32 apply arithmetic as the single-GPU level 0
+    const size_t n32 = size_t(p32_size(wf.grid.d));
+    wf.p32a.alloc(n32);
+    wf.p32b.alloc(n32);
+    wf.p32a.zero(s);
+    wf.p32b.zero(s);
+  }
 
   auto W = std::make_unique<Hier>();
   W->fine = &wf;
@@ -612,7 +713,7 @@ std::unique_ptr<DistPart> dist_build(Hier& F, int n_dist, const int* planes, con
     SG_CUDA(cudaMemcpyAsync(L->diag.p, FL.diag.p + voff, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
     SG_CUDA(cudaMemcpyAsync(L->dinv.p, FL.dinv.p + voff, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
     SG_CUDA(cudaMemcpyAsync(L->dinv32.p, FL.dinv32.p + voff, sizeof(float) * n, cudaMemcpyDeviceToDevice, s));
-    alloc_work(*L);
+    alloc_work(*L, s);
     for (auto* b : {&L->w.r, &L->w.x, &L->w.d64, &L->w.y64, &L->w.dd64}) b->zero(s);
     for (auto* b : {&L->w.b32, &L->w.x32, &L->w.y32, &L->w.dd32}) b->zero(s);
     W->lv.push_back(std::move(L));

@@ -44,6 +44,8 @@ struct CommHooks {
 struct LevelWork {
   DBuf<double> r, x, d64, y64, dd64;
   DBuf<float> b32, x32, y32, dd32;
+  DBuf<float> x32b;        // P32 level: ping-pong partner of x32 for the fused smoother
+  float* xcur = nullptr;   // P32 level: buffer holding the smoother's last FP32 iterate
 };
 
 struct Level {
@@ -58,8 +60,11 @@ struct Level {
   double lam = 0.0;
   DBuf<double> diag, dinv;
   DBuf<float> dinv32;
+  DBuf<float> dinv32p;  // P32 copy of dinv32 (p32 levels)
   LevelWork w;
+  bool p32 = false;  // level-0 FP32 vectors in the P32 layout (sg_fine_pk.cu)
   int64_t nd() const { return 3 * g->d.nnodes(); }
+  int64_t n32() const { return p32_size(g->d); }
 };
 
 struct Hier {

@@ -35,6 +35,7 @@ struct FineOp {
   KwParam<float> kw32;
   bool walsh_ok = false;
   double emax = 0.0;
+  DBuf<float> p32a, p32b;  // P32 staging for node-layout FP32 applies (API path)
 };
 
 // FP64 / FP32 dispatch to the Walsh streaming kernel when the element matrix
@@ -42,6 +43,21 @@ struct FineOp {
 void fine_apply_f64(const FineOp& op, const double* u, double* y, cudaStream_t s);
 void fine_apply_walsh_f32(const FineOp& op, const float* u, float* y, cudaStream_t s);
 void fine_apply_walsh_f64(const FineOp& op, const double* u, double* y, cudaStream_t s);
+// P32 layout (sg_fine_pk.cu): component-planar rows for level-0 FP32 vectors
+int p32_xs(const GridDesc& g);
+int64_t p32_size(const GridDesc& g);
+bool p32_supported(const FineOp& op);
+void fine_apply_p32(const FineOp& op, const float* u, float* y, cudaStream_t s);
+void fine_apply_p32_cheb(const FineOp& op, const float* x, float* xout, const float* b,
+                         const float* dinv, float* d, float A, float AC, bool first, cudaStream_t s);
+void fine_apply_p32_res(const FineOp& op, const float* x, const double* r64, double* out64,
+                        cudaStream_t s);
+template <class Tin>
+void to_p32(const GridDesc& g, const Tin* src, float* dst, cudaStream_t s);
+template <class Tout>
+void from_p32(const GridDesc& g, const float* src, Tout* dst, cudaStream_t s);
+int kKwRowHost(int q);
+int kKwColHost(int q);
 void fine_apply_dense_f32(const FineOp& op, const float* u, float* y, cudaStream_t s);
 void fine_apply_dense_f64(const FineOp& op, const double* u, double* y, cudaStream_t s);
 void fine_apply_f32(const FineOp& op, const float* u, float* y, cudaStream_t s);

@@ -258,3 +258,30 @@ def test_pcg80_brick_matches_range_kernel_100cube(monkeypatch):
     zb, zr = hb.vcycle(r), hr.vcycle(r)
     assert _rel(zb, zr) < 1e-9
     np.testing.assert_array_equal(zb, hb.vcycle(r))  # replay-deterministic
+
+
+@pytest.mark.parametrize("dims,kind", [((100, 100, 100), "uniform"), ((131, 7, 5), "binary"),
+                                       ((9, 33, 17), "random_floor"), ((1, 1, 1), "uniform"),
+                                       ((2, 61, 3), "binary")])
+def test_fine_apply_fp32_packed_tiling(dims, kind):
+    """FP32 apply (packed FP32x2 kernel) across tile shapes: whole-row tiles,
+    x tiles (nx > 126), odd sizes, one element; configs[3] at full size."""
+    g, op, og, E, ke = _pair(dims, kind)
+    u32 = P.SplitMix64(4).gaussian(g.n_free).astype(np.float32)
+    y = op.matvec_tagged(u32, P.PrecisionTag.FP32)
+    assert _rel(y, O.fine_apply(og, E, ke, u32, "fp32")) < 1e-6
+    assert np.array_equal(y, op.matvec_tagged(u32, P.PrecisionTag.FP32))
+
+
+def test_fine_apply_fp32_general_mask():
+    """Non-cantilever Dirichlet mask (per-DOF, grid.py make_grid) on the packed kernel."""
+    nx, ny, nz = 14, 9, 6
+    rng = np.random.default_rng(3)
+    mask = rng.random(3 * (nx + 1) * (ny + 1) * (nz + 1)) < 0.2
+    g = P.make_grid(nx, ny, nz, mask)
+    st = P.make_state("binary", nx, ny, nz, vf=0.5, seed=42)
+    op = P.FineOperator(g, P.simp_modulus(st, 3.0))
+    og = O.make_grid(nx, ny, nz, mask)
+    u32 = P.SplitMix64(8).gaussian(g.n_free).astype(np.float32)
+    y = op.matvec_tagged(u32, P.PrecisionTag.FP32)
+    assert _rel(y, O.fine_apply(og, op.modulus.E, op.ke, u32, "fp32")) < 1e-6
