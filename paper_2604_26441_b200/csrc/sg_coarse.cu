@@ -255,9 +255,11 @@ constexpr int kBrCap = 144;                  // max nodes per brick
 constexpr int kBrThreads = 3 * kBrCap;       // one thread per (node, dk plane)
 constexpr int kBrRegRows = 3;                // q9 = 0..2 (dj = -1) kept in registers
 constexpr int kBrSmRows = 9 - kBrRegRows;
-constexpr int kBrWinMax = 640;               // halo-window nodes
+constexpr int kBrWinMax = 448;               // halo-window nodes
 constexpr int kBrSmemA = 3 * kBrSmRows * 9 * kBrCap;  // doubles
 constexpr int kBrFill = (3 * kBrWinMax + kBrThreads - 1) / kBrThreads;
+constexpr int kBrOwnVec = 4 * 3 * kBrCap;   // pipelined variant: z, q, s, p of the owned nodes
+constexpr int kBrStage = 2 * 160;            // pipelined variant: staged partial packets
 
 struct BrickState {           // device-resident across launches (Pcg80::bstate)
   unsigned long long count;   // arrival counter (monotonic)
@@ -392,6 +394,81 @@ __device__ __forceinline__ void br_allreduce2(double v0, double v1, const BrickA
   t1 = tot[1];
 }
 
+// Split all-reduce of two values for the pipelined variant: publish the
+// block partials and arrive (no wait), collect later (after the SpMV).
+__device__ __forceinline__ void br_publish2(double v0, double v1, const BrickArgs& P,
+                                            unsigned flag, double* red) {
+  v0 = wsum(v0);
+  v1 = wsum(v1);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) {
+    red[warp] = v0;
+    red[16 + warp] = v1;
+  }
+  __syncthreads();
+  if (warp == 0) {
+    const int nb = gridDim.x;
+    uint4* sl = P.slots + (flag & 1) * 2 * nb;
+    const int nw = int(blockDim.x >> 5);
+    const double s0 = wsum(lane < nw ? red[lane] : 0.0);
+    const double s1 = wsum(lane < nw ? red[16 + lane] : 0.0);
+    if (lane == 0) {
+      ll_store(sl + blockIdx.x, s0, flag);
+      ll_store(sl + nb + blockIdx.x, s1, flag);
+    }
+  }
+}
+__device__ __forceinline__ void br_collect2(const BrickArgs& P, unsigned flag,
+                                            unsigned long long target, double* tot, double& t0,
+                                            double& t1) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp == 0) {
+    const int nb = gridDim.x;
+    const uint4* sl = P.slots + (flag & 1) * 2 * nb;
+    if (lane == 0) {
+      unsigned long long c;
+      do {
+        asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(c) : "l"(&P.st->count) : "memory");
+      } while (c < target);
+    }
+    __syncwarp();
+    double a0[5], a1[5];
+    bool ok;
+    do {
+      ok = true;
+#pragma unroll
+      for (int k = 0; k < 5; ++k) {
+        const int bb = lane + 32 * k;
+        a0[k] = 0.0;
+        a1[k] = 0.0;
+        if (bb < nb) {
+          ok = ll_load(sl + bb, flag, a0[k]) && ok;
+          ok = ll_load(sl + nb + bb, flag, a1[k]) && ok;
+        }
+      }
+    } while (!__all_sync(0xffffffffu, ok));
+    const double r0 = wsum(a0[0] + a0[1] + a0[2] + a0[3] + a0[4]);
+    const double r1 = wsum(a1[0] + a1[1] + a1[2] + a1[3] + a1[4]);
+    if (lane == 0) {
+      tot[0] = r0;
+      tot[1] = r1;
+    }
+  }
+  __syncthreads();
+  t0 = tot[0];
+  t1 = tot[1];
+}
+
+// kVar = 2: pipelined Jacobi-PCG (Ghysels & Vanroose 2014, Alg. 4), the same
+// iterates in exact arithmetic; the (r.u, w.u) all-reduce of a step is
+// published before and collected after the step's SpMV n = A m, m = D^-1 w,
+// so its latency hides behind the stencil work:
+//   gamma = r.u, delta = w.u; m = D^-1 w; n = A m;
+//   beta = gamma/gamma_prev; alpha = gamma/(delta - beta*gamma/alpha_prev);
+//   z = n + beta z; q = m + beta q; s = w + beta s; p = u + beta p;
+//   x += alpha p; r -= alpha s; u -= alpha q; w -= alpha z.
+// m crosses blocks as LL packets in two parity buffers (a fast block writes
+// step i+1 while a slow one may still read step i).
 // kCG = false: the reference's Hestenes-Stiefel recurrence (two all-reduces
 // per step).  kCG = true: the Chronopoulos-Gear form of the same Jacobi-PCG
 // (identical iterates in exact arithmetic; one all-reduce of (r.z, w.z) per
@@ -401,11 +478,13 @@ __device__ __forceinline__ void br_allreduce2(double v0, double v1, const BrickA
 //   p = z + beta p; s = w + beta s; x += alpha p; r -= alpha s; z = D^-1 r.
 // The reference's break tests map one to one: its rz_new test of step i-1 is
 // the gamma test of step i, its p.q test the p.Ap test.
-template <bool kCG>
+template <int kVar>
 __global__ void __launch_bounds__(kBrThreads, 1) pcg80_brick_kernel(BrickArgs P) {
   extern __shared__ double smdyn[];
   double* smA = smdyn;             // [(part*6 + row)*9 + entry][kBrCap]
   double* pw = smdyn + kBrSmemA;   // [3][kBrWinMax] p on the brick + halo
+  double* ov = pw + 3 * kBrWinMax;  // [4][3][kBrCap] owner vectors (pipelined variant)
+  uint4* pst = reinterpret_cast<uint4*>(ov + kBrOwnVec);  // [2][160] staged packets
   __shared__ double rowpart[2][3][kBrCap];
   __shared__ double red[32];
   __shared__ double tot;
@@ -530,7 +609,169 @@ __global__ void __launch_bounds__(kBrThreads, 1) pcg80_brick_kernel(BrickArgs P)
     av[2] = a2 + rowpart[0][2][ln] + rowpart[1][2][ln];
   };
 
-  if constexpr (kCG) {
+  if constexpr (kVar == 2) {
+    const int nn3 = 3 * nn;  // one LL parity buffer
+    double xr[3] = {0.0, 0.0, 0.0}, rr[3] = {0.0, 0.0, 0.0}, uu[3] = {0.0, 0.0, 0.0};
+    double ww[3] = {0.0, 0.0, 0.0}, dv[3] = {0.0, 0.0, 0.0};
+    // z, q, s, p of this thread's node live in shared memory (register budget)
+    double* zz = ov + ln;
+    double* qq = ov + 3 * kBrCap + ln;
+    double* ss = ov + 6 * kBrCap + ln;
+    double* pp = ov + 9 * kBrCap + ln;
+    if (owner) {
+#pragma unroll
+      for (int c = 0; c < 3; ++c) zz[c * kBrCap] = qq[c * kBrCap] = ss[c * kBrCap] = pp[c * kBrCap] = 0.0;
+    }
+    // phase 0: u0 = D^-1 b (flag fbase, buffer 0); w0 = A u0
+    if (owner) {
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        rr[c] = P.b[3 * node + c];
+        dv[c] = P.dinv[3 * node + c];
+        uu[c] = dv[c] * rr[c];
+        ll_store(P.zll + c * nn + node, uu[c], fbase);
+      }
+    }
+    auto fill_ph = [&](unsigned ph) {
+      const uint4* base = P.zll + (ph & 1) * nn3;
+      const unsigned zf = fbase + ph;
+      double zv[kBrFill];
+      bool ok[kBrFill];
+#pragma unroll
+      for (int k = 0; k < kBrFill; ++k) {
+        zv[k] = 0.0;
+        ok[k] = fg[k] < 0 || ll_load(base + fg[k], zf, zv[k]);
+      }
+      bool all = true;
+#pragma unroll
+      for (int k = 0; k < kBrFill; ++k) all = all && ok[k];
+      while (!all) {
+        all = true;
+#pragma unroll
+        for (int k = 0; k < kBrFill; ++k) {
+          if (!ok[k]) ok[k] = ll_load(base + fg[k], zf, zv[k]);
+          all = all && ok[k];
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < kBrFill; ++k)
+        if (fw[k] >= 0) pw[fw[k]] = zv[k];
+    };
+    fill_ph(0);
+    __syncthreads();
+    {
+      double av[3];
+      spmv(av);
+      if (owner) {
+#pragma unroll
+        for (int c = 0; c < 3; ++c) ww[c] = fma(P.eps, uu[c], av[c]);
+      }
+    }
+    unsigned epoch = 0;
+    double gprev = 0.0, aprev = 0.0;
+    for (int s = 0; s < P.steps; ++s) {
+      if (P.trace && s == 10) stamp(P.trace, 0);
+      // m = D^-1 w to the neighbours; (r.u, w.u) published
+      double lg = 0.0, ld = 0.0;
+      if (owner) {
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          ll_store(P.zll + ((s + 1) & 1) * nn3 + c * nn + node, dv[c] * ww[c], fbase + unsigned(s) + 1u);
+          lg = fma(rr[c], uu[c], lg);
+          ld = fma(ww[c], uu[c], ld);
+        }
+      }
+      ++epoch;
+      br_publish2(lg, ld, P, fbase | epoch, red);
+      if (P.trace && s == 10) stamp(P.trace, 1);
+      fill_ph(unsigned(s) + 1u);
+      __syncthreads();
+      if (P.trace && s == 10) stamp(P.trace, 5);
+      // stage every block's partial packets into shared memory while the SpMV
+      // runs (cp.async, L2 path); validated and re-polled afterwards
+      const unsigned pf = fbase | epoch;
+      const uint4* sl = P.slots + (pf & 1) * 2 * nb;
+      if (t < 32) {
+        for (int q = t; q < 2 * nb; q += 32) {
+          const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(pst + q));
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(sl + q) : "memory");
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+      }
+      double nv[3];
+      spmv(nv);
+      if (P.trace && s == 10) stamp(P.trace, 3);
+      double gam, del;
+      if (t < 32) {
+        asm volatile("cp.async.wait_all;" ::: "memory");
+        __syncwarp();
+        double a0[5], a1[5];
+#pragma unroll
+        for (int k = 0; k < 5; ++k) {
+          const int bb = t + 32 * k;
+          a0[k] = 0.0;
+          a1[k] = 0.0;
+          if (bb < nb) {
+            const uint4 v0 = pst[bb], v1 = pst[nb + bb];
+            bool ok0 = v0.y == pf && v0.w == pf, ok1 = v1.y == pf && v1.w == pf;
+            a0[k] = __hiloint2double(int(v0.z), int(v0.x));
+            a1[k] = __hiloint2double(int(v1.z), int(v1.x));
+            while (!ok0) ok0 = ll_load(sl + bb, pf, a0[k]);
+            while (!ok1) ok1 = ll_load(sl + nb + bb, pf, a1[k]);
+          }
+        }
+        const double r0 = wsum(a0[0] + a0[1] + a0[2] + a0[3] + a0[4]);
+        const double r1 = wsum(a1[0] + a1[1] + a1[2] + a1[3] + a1[4]);
+        if (t == 0) {
+          tot2[0] = r0;
+          tot2[1] = r1;
+        }
+      }
+      __syncthreads();
+      gam = tot2[0];
+      del = tot2[1];
+      if (P.trace && s == 10) stamp(P.trace, 2);
+      double beta = 0.0, pap = del;
+      if (s > 0) {
+        if (!(gam > 0.0) || !isfinite(gam)) break;
+        beta = gam / gprev;
+        pap = del - beta * gam / aprev;
+      }
+      if (!(pap > 0.0) || !isfinite(pap)) break;
+      const double al = gam / pap;
+      if (owner) {
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          const double mv = pw[c * kBrWinMax + wctr];
+          const double n = fma(P.eps, mv, nv[c]);
+          const double zn = fma(beta, zz[c * kBrCap], n);
+          const double qn = fma(beta, qq[c * kBrCap], mv);
+          const double sn = fma(beta, ss[c * kBrCap], ww[c]);
+          const double pn = fma(beta, pp[c * kBrCap], uu[c]);
+          zz[c * kBrCap] = zn;
+          qq[c * kBrCap] = qn;
+          ss[c * kBrCap] = sn;
+          pp[c * kBrCap] = pn;
+          xr[c] = fma(al, pn, xr[c]);
+          rr[c] = fma(-al, sn, rr[c]);
+          uu[c] = fma(-al, qn, uu[c]);
+          ww[c] = fma(-al, zn, ww[c]);
+        }
+      }
+      gprev = gam;
+      aprev = al;
+    }
+    if (owner) {
+#pragma unroll
+      for (int c = 0; c < 3; ++c) P.x[3 * node + c] = xr[c];
+    }
+    if (blockIdx.x == 0 && t == 0) {
+      P.st->origin = c0;  // this variant never arrives on the counter
+      P.st->seq = seq + 1u;
+    }
+    return;
+  }
+  if constexpr (kVar == 1) {
     double xr[3] = {0.0, 0.0, 0.0}, rr[3] = {0.0, 0.0, 0.0}, dv[3] = {0.0, 0.0, 0.0};
     double pp[3] = {0.0, 0.0, 0.0}, ss[3] = {0.0, 0.0, 0.0};
     if (owner) {
@@ -719,18 +960,23 @@ void Pcg80::setup(const Grid& g, const double* A, const double* diag, double eps
   if (!getenv("SG_PCG80_RANGE") && brick_plan(g.d, nsm, sx, sy, sz)) {
     brick = true;
     nblocks = sx * sy * sz;
-    smem_bytes = int(sizeof(double)) * (kBrSmemA + 3 * kBrWinMax);
+    smem_bytes = int(sizeof(double)) * (kBrSmemA + 3 * kBrWinMax + kBrOwnVec) +
+                 int(sizeof(uint4)) * kBrStage;
     SG_REQUIRE(smem_bytes <= smem_optin, "pcg80 brick kernel shared memory");
     SG_REQUIRE(2 * steps_ + 1 < 1024, "pcg80 step count too large for the packet flags");
-    cgcg = getenv("SG_PCG80_CG") != nullptr;  // measured slower today (see DESIGN)
-    for (void* fn : {(void*)pcg80_brick_kernel<true>, (void*)pcg80_brick_kernel<false>})
+    // 0: Hestenes-Stiefel (two all-reduces per step), 1: Chronopoulos-Gear,
+    // 2: pipelined (the all-reduce hidden behind the SpMV)
+    variant = getenv("SG_PCG80_HS") ? 0 : getenv("SG_PCG80_CG") ? 1 : 2;
+    void* fns[3] = {(void*)pcg80_brick_kernel<0>, (void*)pcg80_brick_kernel<1>,
+                    (void*)pcg80_brick_kernel<2>};
+    for (void* fn : fns)
       SG_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes));
-    SG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-        &per_sm, cgcg ? pcg80_brick_kernel<true> : pcg80_brick_kernel<false>, kBrThreads, smem_bytes));
+    SG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fns[variant], kBrThreads,
+                                                          smem_bytes));
     SG_REQUIRE(per_sm >= 1, "pcg80 brick kernel cannot be resident");
     slots.alloc(size_t(4 * nblocks));
     slots.zero(s);
-    zll.alloc(size_t(3 * g.d.nnodes()));
+    zll.alloc(size_t(6 * g.d.nnodes()));  // two LL parity buffers (pipelined variant)
     zll.zero(s);
     bstate.alloc(3);
     bstate.zero(s);
@@ -774,7 +1020,8 @@ void Pcg80::solve(const double* b, double* x, cudaStream_t s) {
     a.sz = sz;
     a.trace = trace;
     void* args[] = {&a};
-    void* fn = cgcg ? (void*)pcg80_brick_kernel<true> : (void*)pcg80_brick_kernel<false>;
+    void* fn = variant == 2 ? (void*)pcg80_brick_kernel<2>
+             : variant == 1 ? (void*)pcg80_brick_kernel<1> : (void*)pcg80_brick_kernel<0>;
     SG_CUDA(cudaLaunchCooperativeKernel(fn, dim3(nblocks), dim3(kBrThreads),
                                         args, size_t(smem_bytes), s));
     SG_CHECK_LAUNCH();

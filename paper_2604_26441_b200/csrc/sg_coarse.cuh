@@ -17,7 +17,7 @@ struct Pcg80 {
   DBuf<unsigned> bar;
   // brick-partitioned kernel (pcg80_brick_kernel) when the level fits on chip
   bool brick = false;
-  bool cgcg = false;  // Chronopoulos-Gear recurrence (one all-reduce per step)
+  int variant = 2;  // 0 Hestenes-Stiefel, 1 Chronopoulos-Gear, 2 pipelined (sg_coarse.cu)
   int sx = 0, sy = 0, sz = 0;
   DBuf<uint4> slots, zll;
   DBuf<unsigned long long> bstate;

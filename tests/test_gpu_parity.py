@@ -256,7 +256,11 @@ def test_pcg80_brick_matches_range_kernel_100cube(monkeypatch):
         hr = P.build_hierarchy(op, 4, "fp32")
     r = P.SplitMix64(5).gaussian(g.n_free)
     zb, zr = hb.vcycle(r), hr.vcycle(r)
-    assert _rel(zb, zr) < 1e-9
+    # the brick kernel runs the pipelined (Ghysels-Vanroose) recurrence of the
+    # same 80-step Jacobi-PCG; the coarse problem is far from converged after 80
+    # steps, so rounding differences between equivalent recurrences grow to
+    # ~2e-9 here (Hestenes-Stiefel brick vs range: ~2e-11)
+    assert _rel(zb, zr) < 1e-8
     np.testing.assert_array_equal(zb, hb.vcycle(r))  # replay-deterministic
 
 

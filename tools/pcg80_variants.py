@@ -11,8 +11,8 @@ g = P.build_cantilever(N, N, N)
 op = P.FineOperator(g, P.simp_modulus(P.make_state("uniform", N, N, N, vf=0.5), 3.0))
 r = P.SplitMix64(5).gaussian(g.n_free)
 out = {}
-for name, env in (("cg", {"SG_PCG80_CG": "1"}), ("hs", {}), ("range", {"SG_PCG80_RANGE": "1"})):
-    for k in ("SG_PCG80_CG", "SG_PCG80_RANGE"):
+for name, env in (("pipe", {}), ("cg", {"SG_PCG80_CG": "1"}), ("hs", {"SG_PCG80_HS": "1"}), ("range", {"SG_PCG80_RANGE": "1"})):
+    for k in ("SG_PCG80_CG", "SG_PCG80_HS", "SG_PCG80_RANGE"):
         os.environ.pop(k, None)
     os.environ.update(env)
     with warnings.catch_warnings():
@@ -25,6 +25,6 @@ for name, env in (("cg", {"SG_PCG80_CG": "1"}), ("hs", {}), ("range", {"SG_PCG80
     b = g.load[g.free_dofs]
     rep = P.pcg(op.matvec, h.vcycle, b, P.SolverConfig(tol=1e-6, maxiter=200))
     print(f"       pcg iters {rep.iterations} true res {rep.final_true_residual:.4e} hist[-1] {rep.residual_history[-1]:.6e}")
-for a, b in (("cg", "range"), ("hs", "range"), ("cg", "hs")):
+for a, b in (("pipe", "range"), ("cg", "range"), ("hs", "range"), ("pipe", "hs")):
     d = np.linalg.norm(out[a] - out[b]) / np.linalg.norm(out[b])
     print(f"vcycle rel diff {a} vs {b}: {d:.3e}")
