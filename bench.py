@@ -293,6 +293,10 @@ def run_gpu(args):
     tco = prof(3)
     tvc = prof(4)
     tbf = prof(5)
+    try:
+        tch = prof(6)
+    except Exception:
+        tch = None
     peak, peak_kind = _peaks()
     b32 = 8 * n_free + 4 * n_elem
     b64 = 16 * n_free + 8 * n_elem
@@ -300,6 +304,10 @@ def run_gpu(args):
     comps["fine_apply_fp32"] = {"ms": t32, "alg_bytes": b32, "gbs": b32 / t32 / 1e6}
     comps["fine_apply_fp64"] = {"ms": t64, "alg_bytes": b64, "gbs": b64 / t64 / 1e6}
     comps["fine_apply_bf16_tcgen05"] = {"ms": tbf, "alg_bytes": b32, "gbs": b32 / tbf / 1e6}
+    if tch is not None:
+        # fused apply + Chebyshev step: u, E in; b, dinv, d in; d, x' out (FP32)
+        bch = 24 * n_free + 4 * n_elem
+        comps["fine_apply_cheb_fused_fp32"] = {"ms": tch, "alg_bytes": bch, "gbs": bch / tch / 1e6}
     comps["level1_spmv_fp64"] = {"ms": tl1, "alg_bytes": bl1, "gbs": bl1 / tl1 / 1e6}
     comps["coarsest_pcg80"] = {"ms": tco}
     comps["vcycle"] = {"ms": tvc}
@@ -320,7 +328,7 @@ def run_gpu(args):
         "pcg_iters": iters[-1], "final_true_residual": rep.final_true_residual,
         "converged": bool(rep.converged), "setup_s": setup_s,
         "fine_matvec_gbs": achieved,
-        "roofline": {"kernel": "fine_apply_fp32 (fine_apply_walsh_kernel<float>)", "bound": "hbm",
+        "roofline": {"kernel": "fine_apply_fp32 (fine_pk_kernel<0>, packed FP32x2, P32 layout)", "bound": "hbm",
                      "achieved": achieved, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
                      "alg_bytes_per_launch": b32, "launch_ms": t32},

@@ -730,6 +730,13 @@ extern "C" int sg_hier_profile(sg_hier* h, int what, int reps, double* ms_avg, v
         }
         case 4: sg::cycle_run(H, 1, s); break;
         case 5: sg::fine_apply_bf16(*H.fine, fa.p, fb.p, s); break;
+        case 6: {  // the fused level-0 apply + Chebyshev step the V-cycle runs (P32)
+          SG_REQUIRE(H.lv[0]->p32, "level 0 is not in the P32 layout");
+          sg::Level& L = *H.lv[0];
+          sg::fine_apply_p32_cheb(*H.fine, L.w.x32.p, L.w.x32b.p, L.w.b32.p, L.dinv32p.p, L.w.dd32.p,
+                                  0.5f, 0.25f, false, s);
+          break;
+        }
         default: throw sg::Error("unknown profile target");
       }
       SG_CUDA(cudaEventRecord(e1, s));
