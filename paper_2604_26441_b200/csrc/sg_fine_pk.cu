@@ -311,7 +311,13 @@ fine_pk_kernel(GridDesc g, const uint8_t* __restrict__ nmask, const float* __res
               dn.y = __fadd_rn(dn.y, __fmul_rn(ep.AC, dd.y));
             }
             *reinterpret_cast<float2*>(ep.d + o) = dn;
-            *reinterpret_cast<float2*>(ep.xout + o) = make_float2(__fadd_rn(xx.x, dn.x), __fadd_rn(xx.y, dn.y));
+            const float2 xn = make_float2(__fadd_rn(xx.x, dn.x), __fadd_rn(xx.y, dn.y));
+            *reinterpret_cast<float2*>(ep.xout + o) = xn;
+            if (ep.out64) {  // last smoothing step: also the f64 node-layout iterate
+              const int64_t q = 3 * nodei + c;
+              ep.out64[q] = double(xn.x);
+              if (own1) ep.out64[q + 3] = double(xn.y);
+            }
           } else {
             const int64_t q = 3 * nodei + c;
             ep.out64[q] = __dsub_rn(ep.r64[q], double(y0));
@@ -409,8 +415,10 @@ void fine_apply_p32(const FineOp& op, const float* u, float* y, cudaStream_t s) 
   launch_pk<PK_Y>(op, u, y, PkEpi{}, s);
 }
 void fine_apply_p32_cheb(const FineOp& op, const float* x, float* xout, const float* b,
-                         const float* dinv, float* d, float A, float AC, bool first, cudaStream_t s) {
+                         const float* dinv, float* d, float A, float AC, bool first, cudaStream_t s,
+                         double* xout64) {
   PkEpi ep;
+  ep.out64 = xout64;
   ep.b = b;
   ep.dinv = dinv;
   ep.d = d;
@@ -426,6 +434,32 @@ void fine_apply_p32_res(const FineOp& op, const float* x, const double* r64, dou
   ep.r64 = r64;
   ep.out64 = out64;
   launch_pk<PK_RES>(op, x, nullptr, ep, s);
+}
+
+// chebyshev_smooth with x0=None on the P32 level (smoothers.py:90-99):
+// b32 = f32(b64); d = c0*(dinv*b32); x = 0 + d -- one pass from the f64
+// node-layout right-hand side (padding entries written as 0)
+__global__ void cheb_first0_p32_kernel(GridDesc g, int XS, const double* __restrict__ b64,
+                                       const float* __restrict__ dinv, float c0,
+                                       float* __restrict__ b32, float* __restrict__ d,
+                                       float* __restrict__ x, int64_t n) {
+  const int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (q >= n) return;
+  const int i = int(q % XS);
+  const int64_t rc = q / XS;
+  const int c = int(rc % 3);
+  const int64_t node = (rc / 3) * (g.nx + 1) + i;
+  const float bv = i <= g.nx ? __double2float_rn(b64[3 * node + c]) : 0.f;
+  const float dv = __fmul_rn(c0, __fmul_rn(dinv[q], bv));
+  b32[q] = bv;
+  d[q] = dv;
+  x[q] = __fadd_rn(0.f, dv);
+}
+void cheb_first0_p32(const GridDesc& g, const double* b64, const float* dinv, float c0, float* b32,
+                     float* d, float* x, cudaStream_t s) {
+  const int64_t n = int64_t(3) * p32_xs(g) * (g.ny + 1) * (g.nz + 1);
+  cheb_first0_p32_kernel<<<grid_blocks(n, 256), 256, 0, s>>>(g, p32_xs(g), b64, dinv, c0, b32, d, x, n);
+  SG_CHECK_LAUNCH();
 }
 
 // ------------------------------------------------ P32 <-> node conversions

@@ -205,7 +205,7 @@ static void smooth_t(Hier& H, Level& L, const T* b, const double* x0, double* ou
 // the x iterate ping-pongs between x32 and x32b.  Same FP32 rounding points
 // as smooth_t (smoothers.py:90-131).
 static void smooth_p32(Hier& H, Level& L, const double* b64, const double* x0, double* out,
-                       cudaStream_t s) {
+                       cudaStream_t s, bool b_ready = false, bool x0_ready = false) {
   const FineOp& op = *H.fine;
   const GridDesc& g = L.g->d;
   const int64_t n = L.n32();
@@ -214,23 +214,25 @@ static void smooth_p32(Hier& H, Level& L, const double* b64, const double* x0, d
   float* d = L.w.dd32.p;
   float* b = L.w.b32.p;
   const float* dinv = L.dinv32p.p;
-  to_p32<double>(g, b64, b, s);
   static const bool unfused = std::getenv("SG_P32_UNFUSED") != nullptr;  // A/B check
-  int done = 0;
+  bool out_done = false;
   if (L.kind == 0) {  // Chebyshev
     const double lam = L.lam;
     const double sigma = 0.5 * (lam + L.alpha * lam);
     const double delta = 0.5 * (lam - L.alpha * lam);
     const float c0 = float(1.0 / sigma);
+    const int last = L.degree - 1;  // index of the last apply step
     if (!x0) {
-      launch_ew(n, s, [&](int nb, int nt) { cheb_first0_kernel<float><<<nb, nt, 0, s>>>(n, dinv, b, c0, d, x); });
+      cheb_first0_p32(g, b64, dinv, c0, b, d, x, s);  // b32, d, x in one pass
     } else {
-      to_p32<double>(g, x0, x, s);
+      if (!b_ready) to_p32<double>(g, b64, b, s);
+      if (!x0_ready) to_p32<double>(g, x0, x, s);
       if (unfused) {
         fine_apply_p32(op, x, L.w.y32.p, s);
         launch_ew(n, s, [&](int nb, int nt) { cheb_first_kernel<float><<<nb, nt, 0, s>>>(n, dinv, b, L.w.y32.p, c0, d, x); });
       } else {
-        fine_apply_p32_cheb(op, x, xb, b, dinv, d, c0, 0.f, true, s);
+        fine_apply_p32_cheb(op, x, xb, b, dinv, d, c0, 0.f, true, s, last == 0 ? out : nullptr);
+        out_done = last == 0;
         std::swap(x, xb);
       }
     }
@@ -243,29 +245,29 @@ static void smooth_p32(Hier& H, Level& L, const double* b64, const double* x0, d
         const float A = float(a), AC = float(a * c);
         launch_ew(n, s, [&](int nb, int nt) { cheb_step_kernel<float><<<nb, nt, 0, s>>>(n, dinv, b, L.w.y32.p, A, AC, d, x); });
       } else {
-        fine_apply_p32_cheb(op, x, xb, b, dinv, d, float(a), float(a * c), false, s);
+        fine_apply_p32_cheb(op, x, xb, b, dinv, d, float(a), float(a * c), false, s,
+                            it == last ? out : nullptr);
+        out_done = it == last;
         std::swap(x, xb);
       }
     }
-    done = 1;
   } else {  // damped Jacobi: x = x + w*(dinv*(b - Kx))
+    if (!b_ready) to_p32<double>(g, b64, b, s);
     const float w = float(L.omega);
     int steps = L.degree;
     if (!x0) {
       launch_ew(n, s, [&](int nb, int nt) { jac_first0_kernel<float><<<nb, nt, 0, s>>>(n, dinv, b, w, x); });
       steps -= 1;
-    } else {
+    } else if (!x0_ready) {
       to_p32<double>(g, x0, x, s);
     }
     for (int it = 0; it < steps; ++it) {
       fine_apply_p32(op, x, L.w.y32.p, s);
       launch_ew(n, s, [&](int nb, int nt) { jac_step_kernel<float><<<nb, nt, 0, s>>>(n, dinv, b, L.w.y32.p, w, x); });
     }
-    done = 1;
   }
-  (void)done;
   L.w.xcur = x;
-  from_p32<double>(g, x, out, s);
+  if (!out_done) from_p32<double>(g, x, out, s);
 }
 
 void level_smooth(Hier& H, int l, const double* b, const double* x0, double* out, cudaStream_t s) {
@@ -308,9 +310,8 @@ void cycle(Hier& H, int l, int gamma, cudaStream_t s) {
       // (x64 = f64 of it, so the round trip is exact); re-converted after a
       // coarse correction (W-cycle)
       float* xc = L.w.xcur;
-      if (g > 0 || !xc) {
+      if (!xc) {  // W-cycle second pass: x32 = f32(x64) was written by prolong
         xc = L.w.x32.p;
-        to_p32<double>(L.g->d, x64, xc, s);
       }
       fine_apply_p32_res(*H.fine, xc, L.w.r.p, L.w.x.p, s);
     } else {
@@ -320,7 +321,15 @@ void cycle(Hier& H, int l, int gamma, cudaStream_t s) {
     }
     restrict_(*L.g, *C.g, L.w.x.p, C.w.r.p, s);  // L.w.x used as residual scratch here
     cycle(H, l + 1, gamma, s);
-    prolong(*L.g, *C.g, C.w.x.p, x64, /*add=*/true, s);
+    if (L.p32)  // also writes f32(x64) into x32 (P32) for the post-smoother
+      prolong(*L.g, *C.g, C.w.x.p, x64, /*add=*/true, s, L.w.x32.p, p32_xs(L.g->d));
+    else
+      prolong(*L.g, *C.g, C.w.x.p, x64, /*add=*/true, s);
+    L.w.xcur = nullptr;  // x64 changed: a W-cycle's next residual re-converts
+  }
+  if (L.p32) {
+    smooth_p32(H, L, L.w.r.p, x64, L.w.x.p, s, /*b_ready=*/true, /*x0_ready=*/true);
+    return;
   }
   level_smooth(H, l, L.w.r.p, x64, L.w.x.p, s);
 }

@@ -49,7 +49,10 @@ int64_t p32_size(const GridDesc& g);
 bool p32_supported(const FineOp& op);
 void fine_apply_p32(const FineOp& op, const float* u, float* y, cudaStream_t s);
 void fine_apply_p32_cheb(const FineOp& op, const float* x, float* xout, const float* b,
-                         const float* dinv, float* d, float A, float AC, bool first, cudaStream_t s);
+                         const float* dinv, float* d, float A, float AC, bool first, cudaStream_t s,
+                         double* xout64 = nullptr);
+void cheb_first0_p32(const GridDesc& g, const double* b64, const float* dinv, float c0, float* b32,
+                     float* d, float* x, cudaStream_t s);
 void fine_apply_p32_res(const FineOp& op, const float* x, const double* r64, double* out64,
                         cudaStream_t s);
 template <class Tin>
@@ -88,7 +91,7 @@ void diag_floor(const Grid& g, double* d, const double* mean_dev, cudaStream_t s
 // ------------------------------------------------------------- transfers
 // x_f += P x_c (add = true) or x_f = P x_c; node layout, fixed entries zero.
 void prolong(const Grid& fine, const Grid& coarse, const double* xc, double* xf, bool add,
-             cudaStream_t s);
+             cudaStream_t s, float* xp32 = nullptr, int XS = 0);
 void restrict_(const Grid& fine, const Grid& coarse, const double* xf, double* xc,
                cudaStream_t s);
 void transfer_export_csr(const Grid& fine, const Grid& coarse, int64_t* indptr, int64_t* indices,

@@ -12,7 +12,7 @@ namespace sg {
 
 __global__ void prolong_kernel(GridDesc f, GridDesc c, const uint8_t* __restrict__ fmask,
                                const uint8_t* __restrict__ cmask, const double* __restrict__ xc,
-                               double* __restrict__ xf, bool add) {
+                               double* __restrict__ xf, bool add, float* __restrict__ xp32, int XS) {
   const int64_t nn = f.nnodes();
   const int64_t node = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (node >= nn) return;
@@ -38,11 +38,16 @@ __global__ void prolong_kernel(GridDesc f, GridDesc c, const uint8_t* __restrict
 #pragma unroll
   for (int ax = 0; ax < 3; ++ax) {
     double* o = xf + 3 * node + ax;
+    double v;
     if (node_fixed_axis(f, fmask, node, i, ax)) {
+      v = add ? *o : 0.0;
       if (!add) *o = 0.0;
     } else {
-      *o = add ? __dadd_rn(*o, s[ax]) : s[ax];
+      v = add ? __dadd_rn(*o, s[ax]) : s[ax];
+      *o = v;
     }
+    // level-0 P32 copy f32(x) for the post-smoother (sg_fine_pk.cu layout)
+    if (xp32) xp32[((int64_t(k) * FY + j) * 3 + ax) * XS + i] = __double2float_rn(v);
   }
 }
 
@@ -81,10 +86,10 @@ __global__ void restrict_kernel(GridDesc f, GridDesc c, const uint8_t* __restric
 }
 
 void prolong(const Grid& fine, const Grid& coarse, const double* xc, double* xf, bool add,
-             cudaStream_t s) {
+             cudaStream_t s, float* xp32, int XS) {
   const int64_t nn = fine.d.nnodes();
   prolong_kernel<<<grid_blocks(nn, 256), 256, 0, s>>>(fine.d, coarse.d, fine.nmask.p,
-                                                      coarse.nmask.p, xc, xf, add);
+                                                      coarse.nmask.p, xc, xf, add, xp32, XS);
   SG_CHECK_LAUNCH();
 }
 
