@@ -110,6 +110,9 @@ fine_pk_kernel(GridDesc g, const uint8_t* __restrict__ nmask, const float* __res
   // published partials [buf][q][thread]: q 0..2 = i0(row 0), 3..5 = i1(row 0),
   // 6..8 = i2(row 0), 9..11 = i2(row 1), 3 comps each
   __shared__ float pub[2][12][kPkMaxThreads];
+  // PK_CHEB: this plane's b, dinv, x, d of the owned node pair, prefetched
+  // with cp.async at the top of the layer ([q][thread], q = array*3 + comp)
+  extern __shared__ float2 epre[];
   const int t = threadIdx.x, lane = t & 31;
   const int row = t / P, pair = t - row * P;
   const bool live = row < R;
@@ -204,6 +207,21 @@ fine_pk_kernel(GridDesc g, const uint8_t* __restrict__ nmask, const float* __res
     advance(pk >= 0 && pk < g.nz);
     ++pk;
     load_plane();  // prefetch node plane ek+2
+    if constexpr (MODE == PK_CHEB) {
+      if (ek >= k0 && own) {
+        const float* src[4] = {ep.b, ep.dinv, u, ep.d};
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int c = 0; c < 3; ++c) {
+            const unsigned dst = static_cast<unsigned>(
+                __cvta_generic_to_shared(epre + (a * 3 + c) * kPkMaxThreads + t));
+            const float* gp = src[a] + orow + oplane * pl + int64_t(c) * XS;
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(gp) : "memory");
+          }
+      }
+      asm volatile("cp.async.commit_group;" ::: "memory");
+    }
     const float2 En = load_E(ek + 1);
     const bool kin = ek >= 0 && ek < g.nz;
     const float2 Es = mul2(Eraw, make_float2(kin ? m0 : 0.f, kin ? m1 : 0.f));
@@ -279,6 +297,7 @@ fine_pk_kernel(GridDesc g, const uint8_t* __restrict__ nmask, const float* __res
         pub[buf][6 + c][t] = n2[0][c];
         pub[buf][9 + c][t] = n2[1][c];
       }
+      if constexpr (MODE == PK_CHEB) asm volatile("cp.async.wait_group 0;" ::: "memory");
       __syncthreads();
       if (own) {
         const bool left = pair > 0;
@@ -298,15 +317,15 @@ fine_pk_kernel(GridDesc g, const uint8_t* __restrict__ nmask, const float* __res
           if constexpr (MODE == PK_Y) {
             *reinterpret_cast<float2*>(yout + o) = make_float2(y0, y1);
           } else if constexpr (MODE == PK_CHEB) {
-            const float2 bb = *reinterpret_cast<const float2*>(ep.b + o);
-            const float2 di = *reinterpret_cast<const float2*>(ep.dinv + o);
-            const float2 xx = *reinterpret_cast<const float2*>(u + o);
+            const float2 bb = epre[(0 + c) * kPkMaxThreads + t];
+            const float2 di = epre[(3 + c) * kPkMaxThreads + t];
+            const float2 xx = epre[(6 + c) * kPkMaxThreads + t];
             // scalar round-to-nearest intrinsics: never contracted (ptxas
             // was seen fusing even explicit mul.rn/add.rn .f32x2 into FFMA2)
             float2 dn = make_float2(__fmul_rn(ep.A, __fmul_rn(di.x, __fsub_rn(bb.x, y0))),
                                     __fmul_rn(ep.A, __fmul_rn(di.y, __fsub_rn(bb.y, y1))));
             if (!ep.first) {
-              const float2 dd = *reinterpret_cast<const float2*>(ep.d + o);
+              const float2 dd = epre[(9 + c) * kPkMaxThreads + t];
               dn.x = __fadd_rn(dn.x, __fmul_rn(ep.AC, dd.x));
               dn.y = __fadd_rn(dn.y, __fmul_rn(ep.AC, dd.y));
             }
@@ -406,8 +425,15 @@ static void launch_pk(const FineOp& op, const float* u, float* y, const PkEpi& e
   nch = (planes + kchunk - 1) / kchunk;
   const int threads = ((P * R + 31) / 32) * 32;
   dim3 grid(1, tilesy, nch);
-  fine_pk_kernel<MODE><<<grid, threads, 0, s>>>(g, op.grid.nmask.p, u, y, op.E32.p, C, P, R, kchunk,
-                                                p32_xs(g), ep);
+  const size_t dyn = MODE == PK_CHEB ? sizeof(float2) * 12 * kPkMaxThreads : 0;
+  static bool attr_set = false;
+  if (MODE == PK_CHEB && !attr_set) {
+    SG_CUDA(cudaFuncSetAttribute(fine_pk_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 int(dyn)));
+    attr_set = true;
+  }
+  fine_pk_kernel<MODE><<<grid, threads, dyn, s>>>(g, op.grid.nmask.p, u, y, op.E32.p, C, P, R, kchunk,
+                                                  p32_xs(g), ep);
   SG_CHECK_LAUNCH();
 }
 
