@@ -170,7 +170,7 @@ struct Ctx {
       if (r != L0.w.r.p) copy_k<<<nb256(nd), 256, 0, s>>>(nd, r, L0.w.r.p);
       if (sys.dist) dist_cycle(*sys.dist, sys.gamma, s);
       else cycle_run(*sys.hier, sys.gamma, s);
-      copy_k<<<nb256(nd), 256, 0, s>>>(nd, L0.w.x.p, z);
+      if (z != L0.w.x.p) copy_k<<<nb256(nd), 256, 0, s>>>(nd, L0.w.x.p, z);
     } else {
       mul_k<<<nb256(nd), 256, 0, s>>>(nd, sys.fw->diag_inv_ptr(), r, z);
     }
@@ -242,7 +242,11 @@ void pcg_native(NativeSys& sys, const double* b, double* x, const SolverCfg& cfg
     out = SolveOut{1, 0, 0.0, 0, now() - t0};
     return;
   }
-  const View z{C.vec(0)}, p{C.vec(1)}, q{C.vec(2)};
+  // with a hierarchy, r and z ARE the cycle's level-0 input/output vectors
+  // (z is consumed by the r.z reduction and the p update before the next
+  // cycle overwrites it), so M needs no copies
+  const bool alias = sys.hier && !sys.dist;
+  const View z{alias ? sys.hier->lv[0]->w.x.p : C.vec(0)}, p{C.vec(1)}, q{C.vec(2)};
   double* r = sys.hier ? sys.hier->lv[0]->w.r.p : C.vec(3);
   copy_k<<<nb256(nd), 256, 0, s>>>(nd, b, r);
   C.M(r, z.p);
