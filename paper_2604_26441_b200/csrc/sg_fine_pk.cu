@@ -106,7 +106,7 @@ template <int MODE>
 __global__ void __launch_bounds__(kPkMaxThreads, 1)
 fine_pk_kernel(GridDesc g, const uint8_t* __restrict__ nmask, const float* __restrict__ u,
                float* __restrict__ yout, const float* __restrict__ E, PkCoef C, int P, int R,
-               int kchunk, int XS, PkEpi ep) {
+               int kchunk, int XS, int SX, PkEpi ep) {
   // published partials [buf][q][thread]: q 0..2 = i0(row 0), 3..5 = i1(row 0),
   // 6..8 = i2(row 0), 9..11 = i2(row 1), 3 comps each
   __shared__ float pub[2][12][kPkMaxThreads];
@@ -117,7 +117,14 @@ fine_pk_kernel(GridDesc g, const uint8_t* __restrict__ nmask, const float* __res
   const int row = t / P, pair = t - row * P;
   const bool live = row < R;
   const int NX = g.nx + 1, NY = g.ny + 1;
-  const int ex = 2 * pair;  // e0; nodes ex, ex+1, ex+2
+  // x tiles (nx+1 > 128 nodes): tile t starts at node xo = t*SX (even) and
+  // owns nodes [own_lo, own_hi); its first pair (no left neighbour) and last
+  // pair are halo pairs except at the domain ends
+  const int xo = int(blockIdx.x) * SX;
+  const int own_lo = blockIdx.x == 0 ? 0 : xo + 2;
+  const int own_hi = int(blockIdx.x) == int(gridDim.x) - 1 ? g.nx + 1 : xo + 2 * P - 2;
+  const int ex = xo + 2 * pair;  // e0; nodes ex, ex+1, ex+2
+  const int exl = min(ex, XS - 2);  // load column (phantom pairs past the row end read finite data)
   const int ej = int(blockIdx.y) * (R - 1) - 1 + row;
   const int k0 = int(blockIdx.z) * kchunk;
   const int k1 = min(k0 + kchunk, g.nz + 1);  // output node planes [k0, k1)
@@ -130,7 +137,7 @@ fine_pk_kernel(GridDesc g, const uint8_t* __restrict__ nmask, const float* __res
     const int pk = min(max(k0 - 1, 0), g.nz);
 #pragma unroll
     for (int y = 0; y < 2; ++y)
-      up[y] = u + int64_t(pk) * pl + int64_t(3) * XS * min(max(ej + y, 0), g.ny) + ex;
+      up[y] = u + int64_t(pk) * pl + int64_t(3) * XS * min(max(ej + y, 0), g.ny) + exl;
   }
   const bool rowin = live && ej >= 0 && ej < g.ny;
   const float m0 = (rowin && ex < g.nx) ? 1.f : 0.f;
@@ -142,8 +149,8 @@ fine_pk_kernel(GridDesc g, const uint8_t* __restrict__ nmask, const float* __res
 
   // ownership: nodes (ex, ex+1) of node row ej+1
   const int on = ej + 1;
-  const bool own = live && row < R - 1 && on >= 0 && on <= g.ny && ex <= g.nx;
-  const bool own1 = ex + 1 <= g.nx;
+  const bool own = live && row < R - 1 && on >= 0 && on <= g.ny && ex >= own_lo && ex < own_hi;
+  const bool own1 = ex + 1 < own_hi;
   const int64_t orow = int64_t(3) * XS * max(on, 0) + ex + int64_t(k0) * pl;  // + c*XS
   const int64_t onode = int64_t(ex) + int64_t(NX) * max(on, 0) + int64_t(k0) * NX * NY;
 
@@ -156,7 +163,7 @@ fine_pk_kernel(GridDesc g, const uint8_t* __restrict__ nmask, const float* __res
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
         A[y][c] = ldp2(up[y] + c * XS);
-        a2[y][c] = ldp(up[y] + c * XS + (fix ? 2 : 0));
+        a2[y][c] = ldp(up[y] + c * XS + (fix && exl + 2 < XS ? 2 : 0));
       }
   };
   auto plane_q = [&](float2 (&Q)[3][4]) {
@@ -405,7 +412,7 @@ int64_t p32_size(const GridDesc& g) {
 
 bool p32_supported(const FineOp& op) {
   PkCoef C;
-  return op.walsh_ok && op.grid.d.nx + 1 <= 2 * 64 && pk_params(op, C);
+  return op.walsh_ok && pk_params(op, C);
 }
 
 template <int MODE>
@@ -413,18 +420,35 @@ static void launch_pk(const FineOp& op, const float* u, float* y, const PkEpi& e
   PkCoef C;
   SG_REQUIRE(op.walsh_ok && pk_params(op, C), "P32 apply: element matrix lacks the Walsh block form");
   const GridDesc& g = op.grid.d;
-  const int P = (g.nx + 2) / 2;  // pairs covering nodes 0..nx (a phantom element if nx is odd)
-  SG_REQUIRE(P <= 64, "P32 apply: nx too large for a whole-row tile");
+  // x: one tile per row when (nx+2)/2 <= 64 pairs, else T tiles of P pairs
+  // overlapping by two pairs (stride SX = 2P - 4 nodes), P as small as T allows
+  int P = (g.nx + 2) / 2, T = 1, SX = 2 * P;
+  if (P > 64) {
+    for (T = 2;; ++T) {
+      P = (g.nx + 1 + 4 * (T - 1) + 2 * T - 1) / (2 * T);
+      if (P <= 64) break;
+    }
+    SX = 2 * P - 4;
+  }
   int R = std::max(2, kPkMaxThreads / P);
   R = std::min(R, g.ny + 2);
   const int tilesy = (g.ny + 1 + (R - 1) - 1) / (R - 1);
   const int planes = g.nz + 1;
-  // z chunks: fill the SMs once (one CTA per SM), each chunk pays one halo layer
-  int nch = std::max(1, std::min(planes, kNumSMs / std::max(1, tilesy)));
+  // z chunks (one CTA per SM resident): minimise waves x (chunk + halo layer)
+  const int tiles = T * tilesy;
+  int nch = 1;
+  long best = 1L << 60;
+  for (int c = 1; c <= planes; ++c) {
+    const int kc = (planes + c - 1) / c;
+    const int n = (planes + kc - 1) / kc;
+    const long waves = (long(tiles) * n + kNumSMs - 1) / kNumSMs;
+    const long cost = waves * (kc + 1);
+    if (cost < best) { best = cost; nch = n; }
+  }
   const int kchunk = (planes + nch - 1) / nch;
   nch = (planes + kchunk - 1) / kchunk;
   const int threads = ((P * R + 31) / 32) * 32;
-  dim3 grid(1, tilesy, nch);
+  dim3 grid(T, tilesy, nch);
   const size_t dyn = MODE == PK_CHEB ? sizeof(float2) * 12 * kPkMaxThreads : 0;
   static bool attr_set = false;
   if (MODE == PK_CHEB && !attr_set) {
@@ -433,7 +457,7 @@ static void launch_pk(const FineOp& op, const float* u, float* y, const PkEpi& e
     attr_set = true;
   }
   fine_pk_kernel<MODE><<<grid, threads, dyn, s>>>(g, op.grid.nmask.p, u, y, op.E32.p, C, P, R, kchunk,
-                                                  p32_xs(g), ep);
+                                                  p32_xs(g), SX, ep);
   SG_CHECK_LAUNCH();
 }
 

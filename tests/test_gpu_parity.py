@@ -266,7 +266,8 @@ def test_pcg80_brick_matches_range_kernel_100cube(monkeypatch):
 
 @pytest.mark.parametrize("dims,kind", [((100, 100, 100), "uniform"), ((131, 7, 5), "binary"),
                                        ((9, 33, 17), "random_floor"), ((1, 1, 1), "uniform"),
-                                       ((2, 61, 3), "binary")])
+                                       ((2, 61, 3), "binary"), ((200, 3, 2), "binary"),
+                                       ((257, 2, 3), "random_floor"), ((127, 4, 3), "binary")])
 def test_fine_apply_fp32_packed_tiling(dims, kind):
     """FP32 apply (packed FP32x2 kernel) across tile shapes: whole-row tiles,
     x tiles (nx > 126), odd sizes, one element; configs[3] at full size."""
