@@ -270,8 +270,45 @@ static void smooth_p32(Hier& H, Level& L, const double* b64, const double* x0, d
   if (!out_done) from_p32<double>(g, x, out, s);
 }
 
+// FP64 Galerkin level, Chebyshev: every apply fused with its update
+// (stencil_cheb64); iterates alternate between `out` and the y64 scratch so
+// the last lands in `out` and no step reads the buffer it writes.
+static bool smooth_st64(Hier& H, Level& L, const double* b, const double* x0, double* out,
+                        cudaStream_t s) {
+  if (L.is_fine || L.kind != 0 || H.comm || std::getenv("SG_ST64_UNFUSED")) return false;
+  const int64_t n = L.nd();
+  const double lam = L.lam;
+  const double sigma = 0.5 * (lam + L.alpha * lam);
+  const double delta = 0.5 * (lam - L.alpha * lam);
+  const double c0 = 1.0 / sigma;
+  const int D = L.degree;
+  double* d = L.w.dd64.p;
+  double* scratch = L.w.y64.p;
+  if (x0 == out || x0 == scratch) return false;
+  auto buf = [&](int k) { return ((D - k) & 1) ? scratch : out; };  // iterate X_k
+  const double* cur = x0;
+  if (!x0) {
+    double* x1 = buf(1);
+    launch_ew(n, s, [&](int nb, int nt) { cheb_first0_kernel<double><<<nb, nt, 0, s>>>(n, L.dinv.p, b, c0, d, x1); });
+    cur = x1;
+  } else {
+    stencil_cheb64(*L.g, L.st.T64.p, x0, buf(1), b, L.dinv.p, d, c0, 0.0, true, s);
+    cur = buf(1);
+  }
+  double a = 2.0 / sigma;
+  for (int it = 1; it < D; ++it) {
+    const double c = delta * delta * a / 4.0;
+    a = 1.0 / (sigma - c);
+    stencil_cheb64(*L.g, L.st.T64.p, cur, buf(it + 1), b, L.dinv.p, d, a, a * c, false, s);
+    cur = buf(it + 1);
+  }
+  if (D < 1) launch_ew(n, s, [&](int nb, int nt) { copy_kernel<<<nb, nt, 0, s>>>(n, x0, out); });
+  return true;
+}
+
 void level_smooth(Hier& H, int l, const double* b, const double* x0, double* out, cudaStream_t s) {
   Level& L = *H.lv[size_t(l)];
+  if (L.tag == TAG_FP64 && smooth_st64(H, L, b, x0, out, s)) return;
   if (L.p32) {
     smooth_p32(H, L, b, x0, out, s);
     return;
@@ -302,7 +339,9 @@ void cycle(Hier& H, int l, int gamma, cudaStream_t s) {
   double* x64 = L.w.d64.p;  // holds the f64 iterate across the coarse visits
   level_smooth(H, l, L.w.r.p, nullptr, x64, s);
   for (int g = 0; g < gamma; ++g) {
-    if (L.tag == TAG_FP64) {
+    if (L.tag == TAG_FP64 && !L.is_fine && !H.comm && !std::getenv("SG_ST64_UNFUSED")) {
+      stencil_res64(*L.g, L.st.T64.p, x64, L.w.r.p, L.w.x.p, s);  // r - A x in one pass
+    } else if (L.tag == TAG_FP64) {
       level_apply(H, L, TAG_FP64, x64, L.w.y64.p, s);
       launch_ew(n, s, [&](int nb, int nt) { residual_kernel<double><<<nb, nt, 0, s>>>(n, L.w.r.p, L.w.y64.p, L.w.x.p); });
     } else if (L.p32) {

@@ -60,6 +60,11 @@ void to_p32(const GridDesc& g, const Tin* src, float* dst, cudaStream_t s);
 template <class Tout>
 void from_p32(const GridDesc& g, const float* src, Tout* dst, cudaStream_t s);
 int kKwRowHost(int q);
+// fused FP64 stencil apply + Chebyshev step / residual (sg_stencil.cu)
+void stencil_cheb64(const Grid& g, const double* At, const double* x, double* xout, const double* b,
+                    const double* dinv, double* d, double A, double AC, bool first, cudaStream_t s);
+void stencil_res64(const Grid& g, const double* At, const double* x, const double* r, double* out,
+                   cudaStream_t s);
 int kKwColHost(int q);
 void fine_apply_dense_f32(const FineOp& op, const float* u, float* y, cudaStream_t s);
 void fine_apply_dense_f64(const FineOp& op, const double* u, double* y, cudaStream_t s);

@@ -67,6 +67,74 @@ __global__ void __launch_bounds__(128) stencil_apply_kernel(GridDesc g, const T*
   y[3 * node + 2] = s2;
 }
 
+// Fused epilogues for the FP64 Galerkin levels (smoothers.py:90-110 and the
+// hierarchy.py:214 residual, same _rn operations as the elementwise kernels
+// in sg_hier.cu, so the result is bit-identical to apply-then-update):
+//   mode 1: r = b - Ax; d' = A*(dinv*r) [+ AC*d]; x' = x + d'  (x' != x)
+//   mode 2: out = rr - Ax
+__global__ void __launch_bounds__(128) stencil_fused_kernel(GridDesc g, const double* __restrict__ At,
+                                                            const double* __restrict__ x, int mode,
+                                                            const double* __restrict__ b,
+                                                            const double* __restrict__ dinv,
+                                                            double* __restrict__ d, double* __restrict__ xout,
+                                                            double A, double AC, int first) {
+  const int64_t nn = g.nnodes();
+  const int64_t node = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (node >= nn) return;
+  const int NX = g.nx + 1, NY = g.ny + 1;
+  const int64_t NXY = int64_t(NX) * NY;
+  const int i = int(node % NX), j = int((node / NX) % NY), k = int(node / NXY);
+  const int64_t oi[3] = {i > 0 ? -1 : 0, 0, i < g.nx ? 1 : 0};
+  const int64_t oj[3] = {j > 0 ? -NX : 0, 0, j < g.ny ? NX : 0};
+  const int64_t ok[3] = {k > 0 ? -NXY : 0, 0, k < g.nz ? NXY : 0};
+  double s[3] = {0.0, 0.0, 0.0}, xc[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+  for (int slot = 0; slot < 27; ++slot) {
+    const int64_t nb = node + oi[slot % 3] + oj[(slot / 3) % 3] + ok[slot / 9];
+    const double x0 = x[3 * nb], x1 = x[3 * nb + 1], x2 = x[3 * nb + 2];
+    if (slot == 13) {
+      xc[0] = x0;
+      xc[1] = x1;
+      xc[2] = x2;
+    }
+    const double* a = At + (node >> 5) * (243 * 32) + slot * (9 * 32) + (node & 31);
+#pragma unroll
+    for (int r = 0; r < 3; ++r) {
+      s[r] = __dadd_rn(s[r], __dmul_rn(__ldcs(a + (3 * r + 0) * 32), x0));
+      s[r] = __dadd_rn(s[r], __dmul_rn(__ldcs(a + (3 * r + 1) * 32), x1));
+      s[r] = __dadd_rn(s[r], __dmul_rn(__ldcs(a + (3 * r + 2) * 32), x2));
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < 3; ++r) {
+    const int64_t q = 3 * node + r;
+    if (mode == 2) {
+      xout[q] = __dsub_rn(b[q], s[r]);
+    } else {
+      const double rv = __dsub_rn(b[q], s[r]);
+      double dv = __dmul_rn(A, __dmul_rn(dinv[q], rv));
+      if (!first) dv = __dadd_rn(dv, __dmul_rn(AC, d[q]));
+      d[q] = dv;
+      xout[q] = __dadd_rn(xc[r], dv);
+    }
+  }
+}
+
+void stencil_cheb64(const Grid& g, const double* At, const double* x, double* xout, const double* b,
+                    const double* dinv, double* d, double A, double AC, bool first, cudaStream_t s) {
+  const int64_t nn = g.d.nnodes();
+  stencil_fused_kernel<<<grid_blocks(nn, 128), 128, 0, s>>>(g.d, At, x, 1, b, dinv, d, xout, A, AC,
+                                                            first ? 1 : 0);
+  SG_CHECK_LAUNCH();
+}
+void stencil_res64(const Grid& g, const double* At, const double* x, const double* r, double* out,
+                   cudaStream_t s) {
+  const int64_t nn = g.d.nnodes();
+  stencil_fused_kernel<<<grid_blocks(nn, 128), 128, 0, s>>>(g.d, At, x, 2, r, nullptr, nullptr, out,
+                                                            0.0, 0.0, 1);
+  SG_CHECK_LAUNCH();
+}
+
 template <class T>
 void stencil_apply(const Grid& g, const T* At, const T* x, T* y, cudaStream_t s) {
   const int64_t nn = g.d.nnodes();

@@ -290,3 +290,37 @@ def test_fine_apply_fp32_general_mask():
     u32 = P.SplitMix64(8).gaussian(g.n_free).astype(np.float32)
     y = op.matvec_tagged(u32, P.PrecisionTag.FP32)
     assert _rel(y, O.fine_apply(og, op.modulus.E, op.ke, u32, "fp32")) < 1e-6
+
+
+def test_fused_smoothers_bit_identical_to_unfused():
+    """The fused level-0 (P32 apply + Chebyshev / residual) and FP64 stencil
+    (apply + Chebyshev / residual) kernels round exactly like the unfused
+    apply-then-update kernels: V- and W-cycles are bit-identical.  The switches
+    are read once per process, hence the subprocesses."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = (
+        "import sys, warnings, numpy as np; sys.path.insert(0, %r)\n"
+        "import paper_2604_26441_b200 as P\n"
+        "out = {}\n"
+        "for dims, kind, pol in (((16,8,8),'uniform','fp32'), ((12,12,12),'binary','fp32'),"
+        " ((16,16,16),'binary','fp64')):\n"
+        "    g = P.build_cantilever(*dims)\n"
+        "    op = P.FineOperator(g, P.simp_modulus(P.make_state(kind, *dims, vf=0.5, seed=42), 3.0))\n"
+        "    with warnings.catch_warnings():\n"
+        "        warnings.simplefilter('ignore')\n"
+        "        h = P.build_hierarchy(op, 4, pol)\n"
+        "    r = P.SplitMix64(7).gaussian(g.n_free)\n"
+        "    out[str(dims) + kind + 'v'] = h.vcycle(r)\n"
+        "    out[str(dims) + kind + 'w'] = h.wcycle(r)\n"
+        "np.savez(sys.argv[1], **out)\n" % root)
+    res = {}
+    for name, env in (("fused", {}), ("unfused", {"SG_P32_UNFUSED": "1", "SG_ST64_UNFUSED": "1"})):
+        path = os.path.join(root, "gpurun_out", f"_fused_{name}.npz") if os.path.isdir(
+            os.path.join(root, "gpurun_out")) else f"/tmp/_fused_{name}.npz"
+        subprocess.run([sys.executable, "-c", code, path], check=True, env=dict(os.environ, **env))
+        res[name] = np.load(path)
+    for k in res["fused"].files:
+        assert np.array_equal(res["fused"][k], res["unfused"][k]), k
