@@ -577,10 +577,11 @@ __global__ void __launch_bounds__(kBrThreads, 1) pcg80_brick_kernel(BrickArgs P)
       if (fw[k] >= 0) pw[fw[k]] = axpy ? fma(beta, pw[fw[k]], zv[k]) : zv[k];
   };
   // y = K v on the window (the three dk planes summed by the owner thread)
-  auto spmv = [&](double av[3]) {
+  auto spmv_mid = [&](double av[3], auto&& mid) {
     double a0 = 0.0, a1 = 0.0, a2 = 0.0;
 #pragma unroll
     for (int q9 = 0; q9 < 9; ++q9) {
+      if (q9 == 6) mid();  // hook two thirds into the stencil work
       const int w = wbase + (q9 / 3) * WX + q9 % 3;
       const double pv0 = pw[w], pv1 = pw[kBrWinMax + w], pv2 = pw[2 * kBrWinMax + w];
       double a[9];
@@ -608,6 +609,7 @@ __global__ void __launch_bounds__(kBrThreads, 1) pcg80_brick_kernel(BrickArgs P)
     av[1] = a1 + rowpart[0][1][ln] + rowpart[1][1][ln];
     av[2] = a2 + rowpart[0][2][ln] + rowpart[1][2][ln];
   };
+  auto spmv = [&](double av[3]) { spmv_mid(av, [] {}); };
 
   if constexpr (kVar == 2) {
     const int nn3 = 3 * nn;  // one LL parity buffer
@@ -691,15 +693,17 @@ __global__ void __launch_bounds__(kBrThreads, 1) pcg80_brick_kernel(BrickArgs P)
       // runs (cp.async, L2 path); validated and re-polled afterwards
       const unsigned pf = fbase | epoch;
       const uint4* sl = P.slots + (pf & 1) * 2 * nb;
-      if (t < 32) {
-        for (int q = t; q < 2 * nb; q += 32) {
-          const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(pst + q));
-          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(sl + q) : "memory");
-        }
-        asm volatile("cp.async.commit_group;" ::: "memory");
-      }
+      // (issued two thirds into the SpMV, so late publishers are caught)
       double nv[3];
-      spmv(nv);
+      spmv_mid(nv, [&] {
+        if (t < 32) {
+          for (int q = t; q < 2 * nb; q += 32) {
+            const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(pst + q));
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(sl + q) : "memory");
+          }
+          asm volatile("cp.async.commit_group;" ::: "memory");
+        }
+      });
       if (P.trace && s == 10) stamp(P.trace, 3);
       double gam, del;
       if (t < 32) {
