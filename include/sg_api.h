@@ -248,6 +248,17 @@ int sg_vec_div(int dtype, int64_t n, const void* a, double s, void* c, void* str
 /* BF16 round-to-nearest-even on FP32 bits (precision.py:25-48) */
 int sg_vec_bf16(int64_t n, const float* a, float* b, void* stream);
 
+/* ---------------------------------------------------------------------
+ * Host-only work plans (no device needed; used by the CPU tests).
+ * sg_plan_brick: pcg80 brick split of the coarsest node grid -> {sx, sy, sz}
+ *   ({0,0,0}: no split fits, the contiguous-range kernel runs).
+ * sg_plan_p32: level-0 FP32 apply tiling -> {P pairs per tile row, T x tiles,
+ *   SX x-tile stride in nodes, R element rows per y tile, y tiles, kchunk node
+ *   planes per z chunk, z chunks}.
+ * ------------------------------------------------------------------- */
+int sg_plan_brick(int nx, int ny, int nz, int nsm, int32_t* out3);
+int sg_plan_p32(int nx, int ny, int nz, int nsm, int32_t* out7);
+
 #ifdef __cplusplus
 }
 #endif

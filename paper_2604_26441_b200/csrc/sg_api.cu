@@ -796,3 +796,30 @@ int sg_csr_result_get(void* result, int64_t* Cp, int64_t* Cj, double* Cx) {
 void sg_csr_result_free(void* result) { sg::ptap_free(result); }
 
 }  // extern "C"
+
+// Host-only work plans (no device needed): the pcg80 brick split and the P32
+// fine-apply tiling, exposed so their partition invariants are tested on CPU.
+extern "C" int sg_plan_brick(int nx, int ny, int nz, int nsm, int32_t* out3) {
+  return guard([&] {
+    sg::GridDesc g;
+    g.nx = nx;
+    g.ny = ny;
+    g.nz = nz;
+    int sx = 0, sy = 0, sz = 0;
+    const bool ok = sg::brick_plan(g, nsm, sx, sy, sz);
+    out3[0] = ok ? sx : 0;
+    out3[1] = ok ? sy : 0;
+    out3[2] = ok ? sz : 0;
+  });
+}
+extern "C" int sg_plan_p32(int nx, int ny, int nz, int nsm, int32_t* out7) {
+  return guard([&] {
+    sg::GridDesc g;
+    g.nx = nx;
+    g.ny = ny;
+    g.nz = nz;
+    const sg::PkPlan pl = sg::pk_plan(g, nsm);
+    const int v[7] = {pl.P, pl.T, pl.SX, pl.R, pl.tilesy, pl.kchunk, pl.nch};
+    for (int i = 0; i < 7; ++i) out7[i] = v[i];
+  });
+}

@@ -918,7 +918,7 @@ __global__ void __launch_bounds__(kBrThreads, 1) pcg80_brick_kernel(BrickArgs P)
 // Brick split of the node grid for pcg80_brick_kernel: at most nsm bricks of
 // at most kBrCap nodes, halo window <= kBrWinMax; smallest largest brick,
 // then smallest window.  false = no such split (use the range kernel).
-static bool brick_plan(const GridDesc& g, int nsm, int& sx, int& sy, int& sz) {
+bool brick_plan(const GridDesc& g, int nsm, int& sx, int& sy, int& sz) {
   const int NX = g.nx + 1, NY = g.ny + 1, NZ = g.nz + 1;
   long best_b = 1L << 40, best_w = 1L << 40;
   bool found = false;

@@ -27,6 +27,10 @@ struct Pcg80 {
   long long* trace = nullptr;  // development instrumentation (sg_hier_pcg80_trace)
 };
 
+// Brick split of a coarsest grid for the pcg80 brick kernel (host only):
+// sx*sy*sz <= nsm bricks of <= 144 nodes, halo window <= 448 nodes.
+bool brick_plan(const GridDesc& g, int nsm, int& sx, int& sy, int& sz);
+
 // Blocked device Cholesky + explicit inverse of an SPD n x n row-major matrix
 // (sg_dense.cu); returns false on a non-positive pivot.
 bool dense_spd_inverse(int n, double* A, double* Ainv, cudaStream_t s);

@@ -415,13 +415,13 @@ bool p32_supported(const FineOp& op) {
   return op.walsh_ok && pk_params(op, C);
 }
 
-template <int MODE>
-static void launch_pk(const FineOp& op, const float* u, float* y, const PkEpi& ep, cudaStream_t s) {
-  PkCoef C;
-  SG_REQUIRE(op.walsh_ok && pk_params(op, C), "P32 apply: element matrix lacks the Walsh block form");
-  const GridDesc& g = op.grid.d;
-  // x: one tile per row when (nx+2)/2 <= 64 pairs, else T tiles of P pairs
-  // overlapping by two pairs (stride SX = 2P - 4 nodes), P as small as T allows
+// Work plan of the P32 kernel (host only; sg_plan_p32 exposes it for tests).
+// x: one tile per row when (nx+2)/2 <= 64 pairs, else T tiles of P pairs
+// overlapping by two pairs (stride SX = 2P - 4 nodes), P as small as T
+// allows; y: tiles of R element rows overlapping by one; z: chunks of kchunk
+// node planes (+ one recomputed layer) minimising waves x (chunk + 1).
+PkPlan pk_plan(const GridDesc& g, int nsm) {
+  PkPlan pl;
   int P = (g.nx + 2) / 2, T = 1, SX = 2 * P;
   if (P > 64) {
     for (T = 2;; ++T) {
@@ -434,21 +434,31 @@ static void launch_pk(const FineOp& op, const float* u, float* y, const PkEpi& e
   R = std::min(R, g.ny + 2);
   const int tilesy = (g.ny + 1 + (R - 1) - 1) / (R - 1);
   const int planes = g.nz + 1;
-  // z chunks (one CTA per SM resident): minimise waves x (chunk + halo layer)
   const int tiles = T * tilesy;
   int nch = 1;
   long best = 1L << 60;
   for (int c = 1; c <= planes; ++c) {
     const int kc = (planes + c - 1) / c;
     const int n = (planes + kc - 1) / kc;
-    const long waves = (long(tiles) * n + kNumSMs - 1) / kNumSMs;
+    const long waves = (long(tiles) * n + nsm - 1) / nsm;
     const long cost = waves * (kc + 1);
     if (cost < best) { best = cost; nch = n; }
   }
   const int kchunk = (planes + nch - 1) / nch;
   nch = (planes + kchunk - 1) / kchunk;
+  pl.P = P; pl.T = T; pl.SX = SX; pl.R = R; pl.tilesy = tilesy; pl.kchunk = kchunk; pl.nch = nch;
+  return pl;
+}
+
+template <int MODE>
+static void launch_pk(const FineOp& op, const float* u, float* y, const PkEpi& ep, cudaStream_t s) {
+  PkCoef C;
+  SG_REQUIRE(op.walsh_ok && pk_params(op, C), "P32 apply: element matrix lacks the Walsh block form");
+  const GridDesc& g = op.grid.d;
+  const PkPlan pl = pk_plan(g, kNumSMs);
+  const int P = pl.P, R = pl.R, SX = pl.SX, kchunk = pl.kchunk;
   const int threads = ((P * R + 31) / 32) * 32;
-  dim3 grid(T, tilesy, nch);
+  dim3 grid(pl.T, pl.tilesy, pl.nch);
   const size_t dyn = MODE == PK_CHEB ? sizeof(float2) * 12 * kPkMaxThreads : 0;
   static bool attr_set = false;
   if (MODE == PK_CHEB && !attr_set) {

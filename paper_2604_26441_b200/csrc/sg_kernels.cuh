@@ -47,6 +47,10 @@ void fine_apply_walsh_f64(const FineOp& op, const double* u, double* y, cudaStre
 int p32_xs(const GridDesc& g);
 int64_t p32_size(const GridDesc& g);
 bool p32_supported(const FineOp& op);
+struct PkPlan {
+  int P = 0, T = 1, SX = 0, R = 0, tilesy = 0, kchunk = 0, nch = 0;
+};
+PkPlan pk_plan(const GridDesc& g, int nsm);
 void fine_apply_p32(const FineOp& op, const float* u, float* y, cudaStream_t s);
 void fine_apply_p32_cheb(const FineOp& op, const float* x, float* xout, const float* b,
                          const float* dinv, float* d, float A, float AC, bool first, cudaStream_t s,
