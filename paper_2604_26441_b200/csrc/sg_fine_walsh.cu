@@ -87,7 +87,7 @@ constexpr int kWY = 16;   // element columns per tile along y (15 owned nodes)
 constexpr int kWThreads = kWX * kWY;
 
 template <class T>
-__global__ void __launch_bounds__(kWThreads, sizeof(T) == 4 ? 2 : 1)
+__global__ void __launch_bounds__(kWThreads, 2)
 fine_apply_walsh_kernel(GridDesc g, const uint8_t* __restrict__ nmask, const T* __restrict__ u,
                         T* __restrict__ y, const T* __restrict__ E, KwParam<T> P, int kchunk) {
   __shared__ T ex[2][kWY][kWX][6];
