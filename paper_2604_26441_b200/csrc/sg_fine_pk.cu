@@ -505,10 +505,11 @@ __global__ void cheb_first0_p32_kernel(GridDesc g, int XS, const double* __restr
                                        float* __restrict__ x, int64_t n) {
   const int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (q >= n) return;
-  const int i = int(q % XS);
-  const int64_t rc = q / XS;
-  const int c = int(rc % 3);
-  const int64_t node = (rc / 3) * (g.nx + 1) + i;
+  const int q32 = int(q);  // 32-bit index math (P32 vectors < 2^31 entries)
+  const int rc = q32 / XS;
+  const int i = q32 - rc * XS;
+  const int r3 = rc / 3, c = rc - 3 * r3;
+  const int64_t node = int64_t(r3) * (g.nx + 1) + i;
   const float bv = i <= g.nx ? __double2float_rn(b64[3 * node + c]) : 0.f;
   const float dv = __fmul_rn(c0, __fmul_rn(dinv[q], bv));
   b32[q] = bv;
@@ -528,10 +529,11 @@ __global__ void to_p32_kernel(GridDesc g, int XS, const Tin* __restrict__ src, f
                               int64_t n) {
   const int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (q >= n) return;
-  const int i = int(q % XS);
-  const int64_t rc = q / XS;  // (k*NY + j)*3 + c
-  const int c = int(rc % 3);
-  const int64_t node = (rc / 3) * (g.nx + 1) + i;
+  const int q32 = int(q);  // 32-bit index math (P32 vectors < 2^31 entries)
+  const int rc = q32 / XS;
+  const int i = q32 - rc * XS;  // (k*NY + j)*3 + c
+  const int r3 = rc / 3, c = rc - 3 * r3;
+  const int64_t node = int64_t(r3) * (g.nx + 1) + i;
   dst[q] = i <= g.nx ? float(src[3 * node + c]) : 0.f;
 }
 template <class Tout>
@@ -539,11 +541,10 @@ __global__ void from_p32_kernel(GridDesc g, int XS, const float* __restrict__ sr
                                 int64_t nd) {
   const int64_t d = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (d >= nd) return;
-  const int c = int(d % 3);
-  const int64_t node = d / 3;
-  const int i = int(node % (g.nx + 1));
-  const int64_t jk = node / (g.nx + 1);
-  dst[d] = Tout(src[(jk * 3 + c) * XS + i]);
+  const int d32 = int(d), node = d32 / 3, c = d32 - 3 * node;  // 32-bit index math
+  const int jk = node / (g.nx + 1);
+  const int i = node - jk * (g.nx + 1);
+  dst[d] = Tout(src[(int64_t(jk) * 3 + c) * XS + i]);
 }
 template <class Tin>
 void to_p32(const GridDesc& g, const Tin* src, float* dst, cudaStream_t s) {

@@ -42,7 +42,10 @@ __global__ void __launch_bounds__(128) stencil_apply_kernel(GridDesc g, const T*
   if (node >= nn) return;
   const int NX = g.nx + 1, NY = g.ny + 1;
   const int64_t NXY = int64_t(NX) * NY;
-  const int i = int(node % NX), j = int((node / NX) % NY), k = int(node / NXY);
+  // 32-bit index math (node < 2^31 for every level): 64-bit div/mod is a long
+  // software sequence
+  const int nd32 = int(node), jk = nd32 / NX;
+  const int i = nd32 - jk * NX, j = jk % NY, k = jk / NY;
   const int64_t oi[3] = {i > 0 ? -1 : 0, 0, i < g.nx ? 1 : 0};
   const int64_t oj[3] = {j > 0 ? -NX : 0, 0, j < g.ny ? NX : 0};
   const int64_t ok[3] = {k > 0 ? -NXY : 0, 0, k < g.nz ? NXY : 0};
@@ -83,7 +86,10 @@ __global__ void __launch_bounds__(128) stencil_fused_kernel(GridDesc g, const do
   if (node >= nn) return;
   const int NX = g.nx + 1, NY = g.ny + 1;
   const int64_t NXY = int64_t(NX) * NY;
-  const int i = int(node % NX), j = int((node / NX) % NY), k = int(node / NXY);
+  // 32-bit index math (node < 2^31 for every level): 64-bit div/mod is a long
+  // software sequence
+  const int nd32 = int(node), jk = nd32 / NX;
+  const int i = nd32 - jk * NX, j = jk % NY, k = jk / NY;
   const int64_t oi[3] = {i > 0 ? -1 : 0, 0, i < g.nx ? 1 : 0};
   const int64_t oj[3] = {j > 0 ? -NX : 0, 0, j < g.ny ? NX : 0};
   const int64_t ok[3] = {k > 0 ? -NXY : 0, 0, k < g.nz ? NXY : 0};

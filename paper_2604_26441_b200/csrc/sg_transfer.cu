@@ -17,7 +17,8 @@ __global__ void prolong_kernel(GridDesc f, GridDesc c, const uint8_t* __restrict
   const int64_t node = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (node >= nn) return;
   const int FX = f.nx + 1, FY = f.ny + 1, CX = c.nx + 1, CY = c.ny + 1;
-  const int i = int(node % FX), j = int((node / FX) % FY), k = int(node / (int64_t(FX) * FY));
+  const int nd32 = int(node), jk = nd32 / FX;  // 32-bit index math
+  const int i = nd32 - jk * FX, j = jk % FY, k = jk / FY;
   int pi[2], pj[2], pk[2];
   double wi, wj, wk;
   int ni, nj, nk;
@@ -58,7 +59,8 @@ __global__ void restrict_kernel(GridDesc f, GridDesc c, const uint8_t* __restric
   const int64_t node = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (node >= nn) return;
   const int FX = f.nx + 1, FY = f.ny + 1, CX = c.nx + 1, CY = c.ny + 1;
-  const int i = int(node % CX), j = int((node / CX) % CY), k = int(node / (int64_t(CX) * CY));
+  const int nd32 = int(node), jk = nd32 / CX;  // 32-bit index math
+  const int i = nd32 - jk * CX, j = jk % CY, k = jk / CY;
   double s[3] = {0.0, 0.0, 0.0};
   for (int dk = -1; dk <= 1; ++dk) {
     const int fk = 2 * k + dk;
@@ -111,7 +113,8 @@ __global__ void p_rows_kernel(GridDesc f, GridDesc c, int64_t nfree, const int32
   const int FX = f.nx + 1, FY = f.ny + 1, CX = c.nx + 1, CY = c.ny + 1;
   const int64_t node = f2d[r] / 3;
   const int ax = f2d[r] % 3;
-  const int i = int(node % FX), j = int((node / FX) % FY), k = int(node / (int64_t(FX) * FY));
+  const int nd32 = int(node), jk = nd32 / FX;  // 32-bit index math
+  const int i = nd32 - jk * FX, j = jk % FY, k = jk / FY;
   const int ni = (i & 1) ? 2 : 1, nj = (j & 1) ? 2 : 1, nk = (k & 1) ? 2 : 1;
   const double w = ((i & 1) ? 0.5 : 1.0) * ((j & 1) ? 0.5 : 1.0) * ((k & 1) ? 0.5 : 1.0);
   int64_t o = indptr ? indptr[r] : 0, cnt = 0;
