@@ -102,11 +102,16 @@ __device__ __forceinline__ float2 ldp2(const float* p) {
   return v;
 }
 
-template <int MODE>
+// XSC > 0: the row stride is the compile-time constant XSC (P32 rows padded to
+// a multiple of 32 floats), so every address is base + immediate and the
+// per-layer address arithmetic (IMAD on the FMA pipe) disappears; XSC = 0:
+// runtime stride (rows wider than 256 nodes).
+template <int MODE, int XSC>
 __global__ void __launch_bounds__(kPkMaxThreads, 1)
 fine_pk_kernel(GridDesc g, const uint8_t* __restrict__ nmask, const float* __restrict__ u,
                float* __restrict__ yout, const float* __restrict__ E, PkCoef C, int P, int R,
-               int kchunk, int XS, int SX, PkEpi ep) {
+               int kchunk, int XS_, int SX, PkEpi ep) {
+  const int XS = XSC > 0 ? XSC : XS_;
   // published partials [buf][q][thread]: q 0..2 = i0(row 0), 3..5 = i1(row 0),
   // 6..8 = i2(row 0), 9..11 = i2(row 1), 3 comps each
   __shared__ float pub[2][12][kPkMaxThreads];
@@ -405,7 +410,12 @@ static bool pk_params(const FineOp& op, PkCoef& C) {
   return true;
 }
 
-int p32_xs(const GridDesc& g) { return ((g.nx + 1) + 1) & ~1; }
+// Row stride of the P32 layout: NX rounded up to a multiple of 32 floats up to
+// 256 (compile-time strides for the apply kernel), else to even.
+int p32_xs(const GridDesc& g) {
+  const int nx1 = g.nx + 1;
+  return nx1 <= 256 ? (nx1 + 31) & ~31 : (nx1 + 1) & ~1;
+}
 int64_t p32_size(const GridDesc& g) {
   return int64_t(3) * p32_xs(g) * (g.ny + 1) * (g.nz + 1) + 4;  // + slack for the i2 reads
 }
@@ -460,14 +470,29 @@ static void launch_pk(const FineOp& op, const float* u, float* y, const PkEpi& e
   const int threads = ((P * R + 31) / 32) * 32;
   dim3 grid(pl.T, pl.tilesy, pl.nch);
   const size_t dyn = MODE == PK_CHEB ? sizeof(float2) * 12 * kPkMaxThreads : 0;
-  static bool attr_set = false;
-  if (MODE == PK_CHEB && !attr_set) {
-    SG_CUDA(cudaFuncSetAttribute(fine_pk_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 int(dyn)));
-    attr_set = true;
+  const int XS = p32_xs(g);
+  static bool attr_set[9] = {};
+  auto go = [&](auto kern) {
+    const int slot = XS <= 256 && XS % 32 == 0 ? XS / 32 : 0;
+    if (MODE == PK_CHEB && !attr_set[slot]) {
+      SG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(dyn)));
+      attr_set[slot] = true;
+    }
+    kern<<<grid, threads, dyn, s>>>(g, op.grid.nmask.p, u, y, op.E32.p, C, P, R, kchunk, XS, SX, ep);
+  };
+  // (the fused Chebyshev variant keeps the runtime stride: with a constant one
+  // ptxas hoists more offsets and spills; measured slower)
+  switch (MODE == PK_CHEB ? 0 : XS) {
+    case 32: go(fine_pk_kernel<MODE, 32>); break;
+    case 64: go(fine_pk_kernel<MODE, 64>); break;
+    case 96: go(fine_pk_kernel<MODE, 96>); break;
+    case 128: go(fine_pk_kernel<MODE, 128>); break;
+    case 160: go(fine_pk_kernel<MODE, 160>); break;
+    case 192: go(fine_pk_kernel<MODE, 192>); break;
+    case 224: go(fine_pk_kernel<MODE, 224>); break;
+    case 256: go(fine_pk_kernel<MODE, 256>); break;
+    default: go(fine_pk_kernel<MODE, 0>); break;
   }
-  fine_pk_kernel<MODE><<<grid, threads, dyn, s>>>(g, op.grid.nmask.p, u, y, op.E32.p, C, P, R, kchunk,
-                                                  p32_xs(g), SX, ep);
   SG_CHECK_LAUNCH();
 }
 
@@ -510,7 +535,8 @@ __global__ void cheb_first0_p32_kernel(GridDesc g, int XS, const double* __restr
   const int i = q32 - rc * XS;
   const int r3 = rc / 3, c = rc - 3 * r3;
   const int64_t node = int64_t(r3) * (g.nx + 1) + i;
-  const float bv = i <= g.nx ? __double2float_rn(b64[3 * node + c]) : 0.f;
+  if (i > g.nx) return;  // row padding: zero since allocation, never written
+  const float bv = __double2float_rn(b64[3 * node + c]);
   const float dv = __fmul_rn(c0, __fmul_rn(dinv[q], bv));
   b32[q] = bv;
   d[q] = dv;
