@@ -2,7 +2,8 @@
 
 Run in the build container (where /root/reference exists):
 
-    PYTHONDONTWRITEBYTECODE=1 python oracle/make_golden.py
+    PYTHONDONTWRITEBYTECODE=1 python oracle/make_golden.py          # .npz vectors
+    PYTHONDONTWRITEBYTECODE=1 python oracle/make_golden.py bench    # bench_reports.json
 
 It imports ``simpgmg`` from /root/reference/pkg/src (read-only) and writes
 small .npz files.  ``tests/test_oracle_golden.py`` pins ``oracle/simp_oracle.py``
@@ -163,5 +164,43 @@ def main():
     print("wrote", sorted(os.listdir(OUT)))
 
 
+# Specs whose reference reports pin the GPU-backed bench layer
+# (tests/test_bench_layer_*.py): overrides on top of the ExperimentSpec defaults.
+BENCH_SPECS = {
+    "validate": {"experiment": "validate"},
+    "solve": {"experiment": "solve", "grid": (16, 8, 8), "trials": 2, "warmups": 1},
+    "probe": {"experiment": "probe"},
+    "sweep": {"experiment": "sweep"},
+    "sweep_precisions": {"experiment": "sweep", "grids": ((8, 4, 4),), "vfs": (0.5,),
+                         "ps": (3.0,), "precisions": ("fp64", "fp32", "bf16"),
+                         "smoothers": ("chebyshev", "jacobi")},
+    "robustness": {"experiment": "robustness", "restart": 50, "maxiter": 500},
+}
+
+
+def bench_reports():
+    """Reference numeric payloads (wall-clock fields stripped) -> bench_reports.json."""
+    import json
+    from dataclasses import replace
+    sys.path.insert(0, REF)
+    from simpgmg.bench import reports, runner, specs
+    out = {}
+    for name, over in BENCH_SPECS.items():
+        spec = replace(specs.ExperimentSpec(), **over)
+        with warnings.catch_warnings():
+            warnings.simplefilter("ignore")
+            rep = runner.run_experiment(spec)
+        out[name] = {"overrides": json.loads(json.dumps(over)),
+                     "payload": reports.numeric_payload(rep),
+                     "exit_code": runner.exit_code(rep)}
+    with open(os.path.join(OUT, "bench_reports.json"), "w", encoding="utf-8") as fh:
+        json.dump(out, fh, indent=1, sort_keys=True)
+        fh.write("\n")
+    print("wrote bench_reports.json")
+
+
 if __name__ == "__main__":
-    main()
+    if sys.argv[1:] == ["bench"]:
+        bench_reports()
+    else:
+        main()
