@@ -77,7 +77,7 @@ __device__ __forceinline__ double grid_allreduce(double v, const Pcg80Args& P, u
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int nw = int(blockDim.x >> 5);
+  const int nw = int((blockDim.x + 31) >> 5);
   if (lane == 0) sm[warp] = v;
   __syncthreads();
   const int nb = gridDim.x;
@@ -254,12 +254,14 @@ __global__ void __launch_bounds__(kPcgThreads) pcg80_kernel(Pcg80Args P) {
 //    accept a stale packet.
 constexpr int kBrCap = 144;                  // max nodes per brick
 constexpr int kBrThreads = 3 * kBrCap;       // one thread per (node, dk plane)
+constexpr int kBrBlock = (kBrThreads + 31) / 32 * 32;  // full warps (shuffles, tcgen05 .aligned)
+constexpr int kBrLn = kBrCap + (kBrBlock - kBrThreads);  // row pitch of the per-part partials
 constexpr int kBrRegRows = 3;                // q9 = 0..2 (dj = -1) kept in registers
 constexpr int kBrSmRows = 9 - kBrRegRows;
 constexpr int kBrWinMax = 448;               // halo-window nodes
 constexpr int kBrSmemA = 3 * kBrSmRows * 9 * kBrCap;  // doubles
-constexpr int kBrFill = (3 * kBrWinMax + kBrThreads - 1) / kBrThreads;
-constexpr int kBrOwnVec = 4 * 3 * kBrCap;   // pipelined variant: z, q, s, p of the owned nodes
+constexpr int kBrFill = (3 * kBrWinMax + kBrBlock - 1) / kBrBlock;
+constexpr int kBrOwnVec = 9 * kBrLn;        // pipelined variant: [part][comp][kBrLn] SpMV partials
 constexpr int kBrStage = 2 * 160;            // pipelined variant: staged partial packets
 
 struct BrickState {           // device-resident across launches (Pcg80::bstate)
@@ -312,7 +314,7 @@ __device__ __forceinline__ double br_allreduce(double v, const BrickArgs& P, uns
   if (warp == 0) {
     const int nb = gridDim.x;
     uint4* sl = P.slots + (flag & 1) * nb;
-    const double s = wsum(lane < int(blockDim.x >> 5) ? red[lane] : 0.0);
+    const double s = wsum(lane < int((blockDim.x + 31) >> 5) ? red[lane] : 0.0);
     if (lane == 0) {
       ll_store(sl + blockIdx.x, s, flag);
       asm volatile("red.relaxed.gpu.global.add.u64 [%0], 1;" ::"l"(&P.st->count) : "memory");
@@ -355,7 +357,7 @@ __device__ __forceinline__ void br_allreduce2(double v0, double v1, const BrickA
   if (warp == 0) {
     const int nb = gridDim.x;
     uint4* sl = P.slots + (flag & 1) * 2 * nb;
-    const int nw = int(blockDim.x >> 5);
+    const int nw = int((blockDim.x + 31) >> 5);
     const double s0 = wsum(lane < nw ? red[lane] : 0.0);
     const double s1 = wsum(lane < nw ? red[16 + lane] : 0.0);
     if (lane == 0) {
@@ -410,7 +412,7 @@ __device__ __forceinline__ void br_publish2(double v0, double v1, const BrickArg
   if (warp == 0) {
     const int nb = gridDim.x;
     uint4* sl = P.slots + (flag & 1) * 2 * nb;
-    const int nw = int(blockDim.x >> 5);
+    const int nw = int((blockDim.x + 31) >> 5);
     const double s0 = wsum(lane < nw ? red[lane] : 0.0);
     const double s1 = wsum(lane < nw ? red[16 + lane] : 0.0);
     if (lane == 0) {
@@ -460,6 +462,46 @@ __device__ __forceinline__ void br_collect2(const BrickArgs& P, unsigned flag,
   t1 = tot[1];
 }
 
+// Tensor memory as a register-file extension (pipelined variant): the
+// kBrRegRows operator rows a thread used to keep in registers live in its
+// warp's TMEM lanes instead (warp w: lanes 32*(w%4).., columns 64*(w/4)..,
+// one double = two 32-bit columns), read back one 9-entry row at a time with
+// tcgen05.ld right before use.  That frees ~50 registers for the shared-memory
+// load pipeline of the SpMV, which was latency-bound on register pressure.
+constexpr int kBrTmRows = 7;     // q9 = 0..6 (63 doubles = 126 of a warp slot's 128 columns)
+constexpr int kBrTmemCols = 512;  // 4 warp slots x 128 columns per lane quarter
+__device__ __forceinline__ void tm_st18(uint32_t addr, const double (&v)[9]) {
+  uint32_t r[18];
+#pragma unroll
+  for (int e = 0; e < 9; ++e) {
+    r[2 * e] = unsigned(__double2loint(v[e]));
+    r[2 * e + 1] = unsigned(__double2hiint(v[e]));
+  }
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
+      "%14,%15,%16};" ::"r"(addr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]),
+      "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
+      : "memory");
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x2.b32 [%0], {%1,%2};" ::"r"(addr + 16u), "r"(r[16]),
+               "r"(r[17]) : "memory");
+}
+__device__ __forceinline__ void tm_ld18(uint32_t addr, double (&v)[9]) {
+  uint32_t r[18];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,"
+      "%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15])
+      : "r"(addr) : "memory");
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x2.b32 {%0,%1}, [%2];"
+               : "=r"(r[16]), "=r"(r[17]) : "r"(addr + 16u) : "memory");
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int e = 0; e < 9; ++e) v[e] = __hiloint2double(int(r[2 * e + 1]), int(r[2 * e]));
+}
+
 // kVar = 2: pipelined Jacobi-PCG (Ghysels & Vanroose 2014, Alg. 4), the same
 // iterates in exact arithmetic; the (r.u, w.u) all-reduce of a step is
 // published before and collected after the step's SpMV n = A m, m = D^-1 w,
@@ -480,13 +522,13 @@ __device__ __forceinline__ void br_collect2(const BrickArgs& P, unsigned flag,
 // The reference's break tests map one to one: its rz_new test of step i-1 is
 // the gamma test of step i, its p.q test the p.Ap test.
 template <int kVar>
-__global__ void __launch_bounds__(kBrThreads, 1) pcg80_brick_kernel(BrickArgs P) {
+__global__ void __launch_bounds__(kBrBlock, 1) pcg80_brick_kernel(BrickArgs P) {
   extern __shared__ double smdyn[];
   double* smA = smdyn;             // [(part*6 + row)*9 + entry][kBrCap]
   double* pw = smdyn + kBrSmemA;   // [3][kBrWinMax] p on the brick + halo
-  double* ov = pw + 3 * kBrWinMax;  // [4][3][kBrCap] owner vectors (pipelined variant)
+  double* ov = pw + 3 * kBrWinMax;  // [3][3][kBrLn] SpMV partials (pipelined variant)
   uint4* pst = reinterpret_cast<uint4*>(ov + kBrOwnVec);  // [2][160] staged packets
-  __shared__ double rowpart[2][3][kBrCap];
+  __shared__ double rowpart[2][3][kBrLn];
   __shared__ double red[32];
   __shared__ double tot;
   __shared__ double tot2[2];
@@ -500,7 +542,8 @@ __global__ void __launch_bounds__(kBrThreads, 1) pcg80_brick_kernel(BrickArgs P)
   const int nloc = bx * by * bz;
   const int WX = bx + 2, WY = by + 2, WZ = bz + 2, wn = WX * WY * WZ;
   const int t = threadIdx.x;
-  const int part = t / kBrCap, ln = t % kBrCap;
+  // threads past 3*kBrCap (warp padding) are part 2 with ln >= kBrCap: never active
+  const int part = min(t / kBrCap, 2), ln = t - part * kBrCap;
   const bool act = ln < nloc;
   const int lnc = act ? ln : 0;
   const int lx = lnc % bx, ly = (lnc / bx) % by, lz = lnc / (bx * by);
@@ -514,20 +557,45 @@ __global__ void __launch_bounds__(kBrThreads, 1) pcg80_brick_kernel(BrickArgs P)
   const unsigned long long c0 = __ldcg(&P.st->origin);
   const unsigned fbase = (seq + 1u) << 10;
 
-  // operator rows: dj = -1 row of this thread's dk plane in registers, the
-  // rest in shared memory
-  double areg[kBrRegRows * 9];
+  // operator rows: dj = -1 row of this thread's dk plane in registers (TMEM
+  // for the pipelined variant), the rest in shared memory
+  // register (TMEM for the pipelined variant) rows / shared-memory rows
+  constexpr int kRR = kVar == 2 ? kBrTmRows : kBrRegRows, kSR = 9 - kRR;
+  double areg[kRR * 9];
 #pragma unroll
-  for (int q = 0; q < kBrRegRows * 9; ++q)
+  for (int q = 0; q < kRR * 9; ++q)
     areg[q] = act ? __ldg(P.A + int64_t((part * 9 + q / 9) * 9 + q % 9) * nn + node) : 0.0;
-  for (int idx = t; idx < kBrSmemA; idx += blockDim.x) {
+  __shared__ uint32_t tm_base;
+  uint32_t tm_row = 0;  // this warp's TMEM address (lane quarter, column slot)
+  if constexpr (kVar == 2) {
+    const int warp = t >> 5;
+    if (warp == 0) {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                       static_cast<unsigned>(__cvta_generic_to_shared(&tm_base))),
+                   "n"(kBrTmemCols) : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    tm_row = tm_base + (uint32_t((warp & 3) * 32) << 16) + uint32_t((warp >> 2) * 128);
+#pragma unroll
+    for (int q = 0; q < kRR; ++q) {
+      double v[9];
+#pragma unroll
+      for (int e = 0; e < 9; ++e) v[e] = areg[q * 9 + e];
+      tm_st18(tm_row + uint32_t(q * 18), v);
+    }
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+  }
+  for (int idx = t; idx < 3 * kSR * 9 * kBrCap; idx += blockDim.x) {
     const int e = idx / kBrCap, l = idx % kBrCap;
-    const int pp = e / (kBrSmRows * 9), qq = (e / 9) % kBrSmRows, ent = e % 9;
+    const int pp = e / (kSR * 9), qq = (e / 9) % kSR, ent = e % 9;
     double v = 0.0;
     if (l < nloc) {
       const int gx = x0 + l % bx, gy = y0 + (l / bx) % by, gz = z0 + l / (bx * by);
       const int gn = gx + NX * (gy + NY * gz);
-      v = __ldg(P.A + int64_t((pp * 9 + kBrRegRows + qq) * 9 + ent) * nn + gn);
+      v = __ldg(P.A + int64_t((pp * 9 + kRR + qq) * 9 + ent) * nn + gn);
     }
     smA[idx] = v;
   }
@@ -535,7 +603,7 @@ __global__ void __launch_bounds__(kBrThreads, 1) pcg80_brick_kernel(BrickArgs P)
   int fw[kBrFill], fg[kBrFill];
 #pragma unroll
   for (int k = 0; k < kBrFill; ++k) {
-    const int iw = t + k * kBrThreads;
+    const int iw = t + k * kBrBlock;
     fw[k] = -1;
     fg[k] = -1;
     if (iw < 3 * wn) {
@@ -588,8 +656,8 @@ __global__ void __launch_bounds__(kBrThreads, 1) pcg80_brick_kernel(BrickArgs P)
       double a[9];
 #pragma unroll
       for (int e = 0; e < 9; ++e)
-        a[e] = q9 < kBrRegRows ? areg[q9 * 9 + e]
-                               : smA[((part * kBrSmRows + q9 - kBrRegRows) * 9 + e) * kBrCap + ln];
+        a[e] = q9 < kRR ? areg[q9 * 9 + e]
+                               : smA[((part * kSR + q9 - kRR) * 9 + e) * kBrCap + ln];
       a0 = fma(a[0], pv0, a0);
       a0 = fma(a[1], pv1, a0);
       a0 = fma(a[2], pv2, a0);
@@ -613,27 +681,56 @@ __global__ void __launch_bounds__(kBrThreads, 1) pcg80_brick_kernel(BrickArgs P)
   auto spmv = [&](double av[3]) { spmv_mid(av, [] {}); };
 
   if constexpr (kVar == 2) {
+    // Component ownership: thread (part, ln) owns component c = part of node
+    // ln, so the ten per-DOF recurrences are scalars in every thread (no
+    // 3-wide owner arrays: the registers go to the SpMV's load pipeline).
     const int nn3 = 3 * nn;  // one LL parity buffer
-    double xr[3] = {0.0, 0.0, 0.0}, rr[3] = {0.0, 0.0, 0.0}, uu[3] = {0.0, 0.0, 0.0};
-    double ww[3] = {0.0, 0.0, 0.0}, dv[3] = {0.0, 0.0, 0.0};
-    // z, q, s, p of this thread's node live in shared memory (register budget)
-    double* zz = ov + ln;
-    double* qq = ov + 3 * kBrCap + ln;
-    double* ss = ov + 6 * kBrCap + ln;
-    double* pp = ov + 9 * kBrCap + ln;
-    if (owner) {
+    const int c = part;
+    double xr = 0.0, rr = 0.0, uu = 0.0, ww = 0.0, dv = 0.0;
+    double zz = 0.0, qq = 0.0, ss = 0.0, pp = 0.0;
+    double* rp3 = ov;  // [src part][comp][kBrLn] SpMV partials
+    // full row sum of this thread's component: the three dk-plane partials
+    // added in part order (p0 + p1) + p2 by every consumer
+    // (two accumulators per row -- register rows / shared rows -- halve the
+    // dependent DFMA chains)
+    auto spmv_own = [&](auto&& mid) {
+      double acc[2][3] = {{0.0, 0.0, 0.0}, {0.0, 0.0, 0.0}};
 #pragma unroll
-      for (int c = 0; c < 3; ++c) zz[c * kBrCap] = qq[c * kBrCap] = ss[c * kBrCap] = pp[c * kBrCap] = 0.0;
-    }
-    // phase 0: u0 = D^-1 b (flag fbase, buffer 0); w0 = A u0
-    if (owner) {
+      for (int q9 = 0; q9 < 9; ++q9) {
+        if (q9 == 6) mid();
+        const int w = wbase + (q9 / 3) * WX + q9 % 3;
+        const double pv0 = pw[w], pv1 = pw[kBrWinMax + w], pv2 = pw[2 * kBrWinMax + w];
+        double a[9];
+        if (q9 < kRR) {
+          tm_ld18(tm_row + uint32_t(q9 * 18), a);
+        } else {
 #pragma unroll
-      for (int c = 0; c < 3; ++c) {
-        rr[c] = P.b[3 * node + c];
-        dv[c] = P.dinv[3 * node + c];
-        uu[c] = dv[c] * rr[c];
-        ll_store(P.zll + c * nn + node, uu[c], fbase);
+          for (int e = 0; e < 9; ++e)
+            a[e] = smA[((part * kSR + q9 - kRR) * 9 + e) * kBrCap + ln];
+        }
+        double* h = acc[q9 & 1];
+        h[0] = fma(a[0], pv0, h[0]);
+        h[0] = fma(a[1], pv1, h[0]);
+        h[0] = fma(a[2], pv2, h[0]);
+        h[1] = fma(a[3], pv0, h[1]);
+        h[1] = fma(a[4], pv1, h[1]);
+        h[1] = fma(a[5], pv2, h[1]);
+        h[2] = fma(a[6], pv0, h[2]);
+        h[2] = fma(a[7], pv1, h[2]);
+        h[2] = fma(a[8], pv2, h[2]);
       }
+      rp3[(part * 3 + 0) * kBrLn + ln] = acc[0][0] + acc[1][0];
+      rp3[(part * 3 + 1) * kBrLn + ln] = acc[0][1] + acc[1][1];
+      rp3[(part * 3 + 2) * kBrLn + ln] = acc[0][2] + acc[1][2];
+      __syncthreads();
+      return (rp3[c * kBrLn + ln] + rp3[(3 + c) * kBrLn + ln]) + rp3[(6 + c) * kBrLn + ln];
+    };
+    // phase 0: u0 = D^-1 b (flag fbase, buffer 0); w0 = A u0
+    if (act) {
+      rr = P.b[3 * node + c];
+      dv = P.dinv[3 * node + c];
+      uu = dv * rr;
+      ll_store(P.zll + c * nn + node, uu, fbase);
     }
     auto fill_ph = [&](unsigned ph) {
       const uint4* base = P.zll + (ph & 1) * nn3;
@@ -663,12 +760,8 @@ __global__ void __launch_bounds__(kBrThreads, 1) pcg80_brick_kernel(BrickArgs P)
     fill_ph(0);
     __syncthreads();
     {
-      double av[3];
-      spmv(av);
-      if (owner) {
-#pragma unroll
-        for (int c = 0; c < 3; ++c) ww[c] = fma(P.eps, uu[c], av[c]);
-      }
+      const double av = spmv_own([] {});
+      if (act) ww = fma(P.eps, uu, av);
     }
     unsigned epoch = 0;
     double gprev = 0.0, aprev = 0.0;
@@ -676,13 +769,10 @@ __global__ void __launch_bounds__(kBrThreads, 1) pcg80_brick_kernel(BrickArgs P)
       if (P.trace && s == 10) stamp(P.trace, 0);
       // m = D^-1 w to the neighbours; (r.u, w.u) published
       double lg = 0.0, ld = 0.0;
-      if (owner) {
-#pragma unroll
-        for (int c = 0; c < 3; ++c) {
-          ll_store(P.zll + ((s + 1) & 1) * nn3 + c * nn + node, dv[c] * ww[c], fbase + unsigned(s) + 1u);
-          lg = fma(rr[c], uu[c], lg);
-          ld = fma(ww[c], uu[c], ld);
-        }
+      if (act) {
+        ll_store(P.zll + ((s + 1) & 1) * nn3 + c * nn + node, dv * ww, fbase + unsigned(s) + 1u);
+        lg = rr * uu;
+        ld = ww * uu;
       }
       ++epoch;
       br_publish2(lg, ld, P, fbase | epoch, red);
@@ -695,8 +785,7 @@ __global__ void __launch_bounds__(kBrThreads, 1) pcg80_brick_kernel(BrickArgs P)
       const unsigned pf = fbase | epoch;
       const uint4* sl = P.slots + (pf & 1) * 2 * nb;
       // (issued two thirds into the SpMV, so late publishers are caught)
-      double nv[3];
-      spmv_mid(nv, [&] {
+      const double nv = spmv_own([&] {
         if (t < 32) {
           for (int q = t; q < 2 * nb; q += 32) {
             const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(pst + q));
@@ -744,36 +833,31 @@ __global__ void __launch_bounds__(kBrThreads, 1) pcg80_brick_kernel(BrickArgs P)
       }
       if (!(pap > 0.0) || !isfinite(pap)) break;
       const double al = gam / pap;
-      if (owner) {
-#pragma unroll
-        for (int c = 0; c < 3; ++c) {
-          const double mv = pw[c * kBrWinMax + wctr];
-          const double n = fma(P.eps, mv, nv[c]);
-          const double zn = fma(beta, zz[c * kBrCap], n);
-          const double qn = fma(beta, qq[c * kBrCap], mv);
-          const double sn = fma(beta, ss[c * kBrCap], ww[c]);
-          const double pn = fma(beta, pp[c * kBrCap], uu[c]);
-          zz[c * kBrCap] = zn;
-          qq[c * kBrCap] = qn;
-          ss[c * kBrCap] = sn;
-          pp[c * kBrCap] = pn;
-          xr[c] = fma(al, pn, xr[c]);
-          rr[c] = fma(-al, sn, rr[c]);
-          uu[c] = fma(-al, qn, uu[c]);
-          ww[c] = fma(-al, zn, ww[c]);
-        }
+      if (act) {
+        const double mv = pw[c * kBrWinMax + wctr];
+        const double n = fma(P.eps, mv, nv);
+        zz = fma(beta, zz, n);
+        qq = fma(beta, qq, mv);
+        ss = fma(beta, ss, ww);
+        pp = fma(beta, pp, uu);
+        xr = fma(al, pp, xr);
+        rr = fma(-al, ss, rr);
+        uu = fma(-al, qq, uu);
+        ww = fma(-al, zz, ww);
       }
       gprev = gam;
       aprev = al;
     }
-    if (owner) {
-#pragma unroll
-      for (int c = 0; c < 3; ++c) P.x[3 * node + c] = xr[c];
-    }
+    if (act) P.x[3 * node + c] = xr;
     if (blockIdx.x == 0 && t == 0) {
       P.st->origin = c0;  // this variant never arrives on the counter
       P.st->seq = seq + 1u;
     }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    if (t < 32)
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tm_base),
+                   "n"(kBrTmemCols) : "memory");
     return;
   }
   if constexpr (kVar == 1) {
@@ -983,7 +1067,7 @@ void Pcg80::setup(const Grid& g, const double* A, const double* diag, double eps
                     (void*)pcg80_brick_kernel<2>};
     for (void* fn : fns)
       SG_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes));
-    SG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fns[variant], kBrThreads,
+    SG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fns[variant], kBrBlock,
                                                           smem_bytes));
     SG_REQUIRE(per_sm >= 1, "pcg80 brick kernel cannot be resident");
     slots.alloc(size_t(4 * nblocks));
@@ -1034,7 +1118,7 @@ void Pcg80::solve(const double* b, double* x, cudaStream_t s) {
     void* args[] = {&a};
     void* fn = variant == 2 ? (void*)pcg80_brick_kernel<2>
              : variant == 1 ? (void*)pcg80_brick_kernel<1> : (void*)pcg80_brick_kernel<0>;
-    SG_CUDA(cudaLaunchCooperativeKernel(fn, dim3(nblocks), dim3(kBrThreads),
+    SG_CUDA(cudaLaunchCooperativeKernel(fn, dim3(nblocks), dim3(kBrBlock),
                                         args, size_t(smem_bytes), s));
     SG_CHECK_LAUNCH();
     return;
