@@ -470,6 +470,7 @@ __device__ __forceinline__ void br_collect2(const BrickArgs& P, unsigned flag,
 // load pipeline of the SpMV, which was latency-bound on register pressure.
 constexpr int kBrTmRows = 7;     // q9 = 0..6 (63 doubles = 126 of a warp slot's 128 columns)
 constexpr int kBrTmemCols = 512;  // 4 warp slots x 128 columns per lane quarter
+constexpr int kMidQ = 4;  // SpMV row at which the partial packets are staged (2..4 best, 8: +2%)
 __device__ __forceinline__ void tm_st18(uint32_t addr, const double (&v)[9]) {
   uint32_t r[18];
 #pragma unroll
@@ -697,7 +698,7 @@ __global__ void __launch_bounds__(kBrBlock, 1) pcg80_brick_kernel(BrickArgs P) {
       double acc[2][3] = {{0.0, 0.0, 0.0}, {0.0, 0.0, 0.0}};
 #pragma unroll
       for (int q9 = 0; q9 < 9; ++q9) {
-        if (q9 == 6) mid();
+        if (q9 == kMidQ) mid();
         const int w = wbase + (q9 / 3) * WX + q9 % 3;
         const double pv0 = pw[w], pv1 = pw[kBrWinMax + w], pv2 = pw[2 * kBrWinMax + w];
         double a[9];
