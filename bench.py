@@ -263,6 +263,8 @@ def run_gpu(args):
     b_pin = torch.from_numpy(b_host).pin_memory()
     x_pin = torch.empty_like(b_pin).pin_memory()
     e2e = []
+    rep_h = solve(b_pin)  # untimed warm-up of the host-buffer path
+    x_pin.copy_(rep_h.x, non_blocking=False)
     for k in range(max(3, min(args.steps, 5))):
         flush.zero_()
         torch.cuda.synchronize()
