@@ -38,13 +38,22 @@ struct PcgStep {  // x += a p; r -= a q; rr
   const double* q;
   const double* sc;
   __device__ void operator()(int64_t i, double (&acc)[1]) const {
+    const Ctx c = prep();
+    use(i, load(i), c, acc);
+  }
+  struct V { double x, r, p, q; };
+  struct Ctx { double a; bool ok; };
+  __device__ Ctx prep() const {  // the step length once per thread, not per element
     const double pq = sc[S_PQ], rz = sc[S_RZ];
     const bool ok = isfinite(pq) && pq != 0.0 && isfinite(rz);
-    double rv = r[i];
-    if (ok) {
-      const double a = __ddiv_rn(rz, pq);
-      x[i] = __dadd_rn(x[i], __dmul_rn(a, p[i]));
-      rv = __dsub_rn(rv, __dmul_rn(a, q[i]));
+    return {ok ? __ddiv_rn(rz, pq) : 0.0, ok};
+  }
+  __device__ V load(int64_t i) const { return {x[i], r[i], __ldg(p + i), __ldg(q + i)}; }
+  __device__ void use(int64_t i, const V& v, const Ctx& c, double (&acc)[1]) const {
+    double rv = v.r;
+    if (c.ok) {
+      x[i] = __dadd_rn(v.x, __dmul_rn(c.a, v.p));
+      rv = __dsub_rn(rv, __dmul_rn(c.a, v.q));
       r[i] = rv;
     }
     acc[0] += rv * rv;

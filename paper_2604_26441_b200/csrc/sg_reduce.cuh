@@ -6,6 +6,7 @@
 // size (fixed per n), never on block scheduling -- the reference's
 // determinism contract (test_acceptance.py:244-257).
 #pragma once
+#include <type_traits>
 #include "sg_common.cuh"
 
 namespace sg {
@@ -57,6 +58,37 @@ __device__ __forceinline__ void block_sum(double (&v)[NV], double* smem /* NV*8 
 
 // F: __device__ void operator()(int64_t i, double (&acc)[NV]) const  (adds into acc)
 // Post: __device__ void operator()(const double (&tot)[NV]) const    (run once, thread 0 of last block)
+//
+// Split functors (the hot PCG ones) also define V (an element's loaded
+// operands), Ctx (per-thread constants, e.g. a step length computed once
+// instead of per element), prep(), load(i) and use(i, v, ctx, acc): the
+// kernel then issues four elements' loads before accumulating them -- in the
+// same order as the plain loop, so the result bits are unchanged.
+template <class F, class = void>
+struct SplitRed : std::false_type {};
+template <class F>
+struct SplitRed<F, std::void_t<typename F::V>> : std::true_type {};
+
+template <int NV, class F>
+__device__ __forceinline__ void red_loop(const F& f, int64_t n, double (&acc)[NV]) {
+  const int64_t stride = int64_t(gridDim.x) * kRedThreads;
+  int64_t i = int64_t(blockIdx.x) * kRedThreads + threadIdx.x;
+  if constexpr (SplitRed<F>::value) {
+    const typename F::Ctx ctx = f.prep();
+    for (; i + 3 * stride < n; i += 4 * stride) {
+      const typename F::V v0 = f.load(i), v1 = f.load(i + stride), v2 = f.load(i + 2 * stride),
+                          v3 = f.load(i + 3 * stride);
+      f.use(i, v0, ctx, acc);
+      f.use(i + stride, v1, ctx, acc);
+      f.use(i + 2 * stride, v2, ctx, acc);
+      f.use(i + 3 * stride, v3, ctx, acc);
+    }
+    for (; i < n; i += stride) f.use(i, f.load(i), ctx, acc);
+  } else {
+    for (; i < n; i += stride) f(i, acc);
+  }
+}
+
 template <int NV, class F, class Post>
 __global__ void __launch_bounds__(kRedThreads) reduce_kernel(int64_t n, F f, Post post,
                                                              double* partials, unsigned* counter) {
@@ -65,8 +97,7 @@ __global__ void __launch_bounds__(kRedThreads) reduce_kernel(int64_t n, F f, Pos
   double acc[NV];
 #pragma unroll
   for (int k = 0; k < NV; ++k) acc[k] = 0.0;
-  const int64_t stride = int64_t(gridDim.x) * kRedThreads;
-  for (int64_t i = int64_t(blockIdx.x) * kRedThreads + threadIdx.x; i < n; i += stride) f(i, acc);
+  red_loop<NV>(f, n, acc);
   block_sum<NV>(acc, smem);
   if (threadIdx.x == 0) {
 #pragma unroll
