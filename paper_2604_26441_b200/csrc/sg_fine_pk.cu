@@ -212,11 +212,10 @@ fine_pk_kernel(GridDesc g, const uint8_t* __restrict__ nmask, const float* __res
     const int64_t eo = int64_t(min(max(ek, 0), g.nz - 1)) * estride;
     return make_float2(ldp(Ep0 + eo), ldp(Ep1 + eo));
   };
-  // one element layer ek: QL holds node plane ek's x/y stage, QH receives
-  // plane ek+1's; the caller alternates the two arrays (loop unrolled by two)
-  // so no per-layer register copies are needed
-  auto layer = [&](int ek, float2 (&QL)[3][4], float2 (&QH)[3][4], const float2 Eraw, float2& Enext) {
-    plane_q(QH);  // node plane ek+1
+  float2 Eraw = load_E(k0 - 1);
+
+  for (int ek = k0 - 1; ek < k1; ++ek) {
+    plane_q(Qhi);  // node plane ek+1
     advance(pk >= 0 && pk < g.nz);
     ++pk;
     load_plane();  // prefetch node plane ek+2
@@ -235,7 +234,7 @@ fine_pk_kernel(GridDesc g, const uint8_t* __restrict__ nmask, const float* __res
       }
       asm volatile("cp.async.commit_group;" ::: "memory");
     }
-    Enext = load_E(ek + 1);
+    const float2 En = load_E(ek + 1);
     const bool kin = ek >= 0 && ek < g.nz;
     const float2 Es = mul2(Eraw, make_float2(kin ? m0 : 0.f, kin ? m1 : 0.f));
     const float2 kA = mul2(Es, make_float2(C.amb, C.amb)), kB = mul2(Es, make_float2(C.b, C.b));
@@ -247,9 +246,9 @@ fine_pk_kernel(GridDesc g, const uint8_t* __restrict__ nmask, const float* __res
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
 #pragma unroll
-      for (int m = 1; m < 4; ++m) v[3 * m + c] = add2(QL[c][m], QH[c][m]);
+      for (int m = 1; m < 4; ++m) v[3 * m + c] = add2(Qlo[c][m], Qhi[c][m]);
 #pragma unroll
-      for (int m = 0; m < 4; ++m) v[3 * (m + 4) + c] = sub2(QL[c][m], QH[c][m]);
+      for (int m = 0; m < 4; ++m) v[3 * (m + 4) + c] = sub2(Qlo[c][m], Qhi[c][m]);
     }
     // w = (E Kw) v, block form
     float2 w[24];
@@ -360,26 +359,11 @@ fine_pk_kernel(GridDesc g, const uint8_t* __restrict__ nmask, const float* __res
       ++oplane;
       buf ^= 1;
     }
-  };
-  float2 Ea = load_E(k0 - 1), Eb;
-  if constexpr (MODE == PK_CHEB) {
-    // (the fused smoother's epilogue leaves no registers for the unrolled
-    // form: it spilled, 33 -> 43 us at 100^3)
-    for (int ek = k0 - 1; ek < k1; ++ek) {
-      layer(ek, Qlo, Qhi, Ea, Eb);
 #pragma unroll
-      for (int c = 0; c < 3; ++c)
+    for (int c = 0; c < 3; ++c)
 #pragma unroll
-        for (int m = 0; m < 4; ++m) Qlo[c][m] = Qhi[c][m];
-      Ea = Eb;
-    }
-  } else {
-    int ek = k0 - 1;
-    for (; ek + 1 < k1; ek += 2) {
-      layer(ek, Qlo, Qhi, Ea, Eb);
-      layer(ek + 1, Qhi, Qlo, Eb, Ea);
-    }
-    if (ek < k1) layer(ek, Qlo, Qhi, Ea, Eb);
+      for (int m = 0; m < 4; ++m) Qlo[c][m] = Qhi[c][m];
+    Eraw = En;
   }
 }
 

@@ -306,7 +306,7 @@ def test_fused_smoothers_bit_identical_to_unfused():
         "import paper_2604_26441_b200 as P\n"
         "out = {}\n"
         "for dims, kind, pol in (((16,8,8),'uniform','fp32'), ((12,12,12),'binary','fp32'),"
-        " ((16,16,16),'binary','fp64')):\n"
+        " ((16,16,16),'binary','fp64'), ((64,48,40),'random_floor','fp32')):\n"
         "    g = P.build_cantilever(*dims)\n"
         "    op = P.FineOperator(g, P.simp_modulus(P.make_state(kind, *dims, vf=0.5, seed=42), 3.0))\n"
         "    with warnings.catch_warnings():\n"
