@@ -523,29 +523,49 @@ void fine_apply_p32_res(const FineOp& op, const float* x, const double* r64, dou
 
 // chebyshev_smooth with x0=None on the P32 level (smoothers.py:90-99):
 // b32 = f32(b64); d = c0*(dinv*b32); x = 0 + d -- one pass from the f64
-// node-layout right-hand side (padding entries written as 0)
+// node-layout right-hand side.  A thread takes an x-pair of nodes: its six
+// contiguous doubles in, one aligned float2 per component and array out
+// (padding entries are never written: zero since allocation).
 __global__ void cheb_first0_p32_kernel(GridDesc g, int XS, const double* __restrict__ b64,
                                        const float* __restrict__ dinv, float c0,
                                        float* __restrict__ b32, float* __restrict__ d,
-                                       float* __restrict__ x, int64_t n) {
-  const int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (q >= n) return;
-  const int q32 = int(q);  // 32-bit index math (P32 vectors < 2^31 entries)
-  const int rc = q32 / XS;
-  const int i = q32 - rc * XS;
-  const int r3 = rc / 3, c = rc - 3 * r3;
-  const int64_t node = int64_t(r3) * (g.nx + 1) + i;
-  if (i > g.nx) return;  // row padding: zero since allocation, never written
-  const float bv = __double2float_rn(b64[3 * node + c]);
-  const float dv = __fmul_rn(c0, __fmul_rn(dinv[q], bv));
-  b32[q] = bv;
-  d[q] = dv;
-  x[q] = __fadd_rn(0.f, dv);
+                                       float* __restrict__ x, int npr, int64_t npairs) {
+  const int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t >= npairs) return;
+  const int t32 = int(t);  // 32-bit index math (pairs < 2^31)
+  const int jk = t32 / npr;
+  const int i0 = 2 * (t32 - jk * npr);
+  const bool two = i0 + 1 <= g.nx;
+  const int64_t node = int64_t(jk) * (g.nx + 1) + i0;
+  const double* bp = b64 + 3 * node;
+  double bv[6];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) bv[k] = bp[k];
+#pragma unroll
+  for (int k = 3; k < 6; ++k) bv[k] = two ? bp[k] : 0.0;
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    const int64_t q = (int64_t(jk) * 3 + c) * XS + i0;
+    const float2 di = *reinterpret_cast<const float2*>(dinv + q);
+    const float b0 = __double2float_rn(bv[c]), b1 = __double2float_rn(bv[3 + c]);
+    const float d0 = __fmul_rn(c0, __fmul_rn(di.x, b0)), d1 = __fmul_rn(c0, __fmul_rn(di.y, b1));
+    if (two) {
+      *reinterpret_cast<float2*>(b32 + q) = make_float2(b0, b1);
+      *reinterpret_cast<float2*>(d + q) = make_float2(d0, d1);
+      *reinterpret_cast<float2*>(x + q) = make_float2(__fadd_rn(0.f, d0), __fadd_rn(0.f, d1));
+    } else {
+      b32[q] = b0;
+      d[q] = d0;
+      x[q] = __fadd_rn(0.f, d0);
+    }
+  }
 }
 void cheb_first0_p32(const GridDesc& g, const double* b64, const float* dinv, float c0, float* b32,
                      float* d, float* x, cudaStream_t s) {
-  const int64_t n = int64_t(3) * p32_xs(g) * (g.ny + 1) * (g.nz + 1);
-  cheb_first0_p32_kernel<<<grid_blocks(n, 256), 256, 0, s>>>(g, p32_xs(g), b64, dinv, c0, b32, d, x, n);
+  const int npr = (g.nx + 2) / 2;  // node pairs per row
+  const int64_t npairs = int64_t(npr) * (g.ny + 1) * (g.nz + 1);
+  cheb_first0_p32_kernel<<<grid_blocks(npairs, 256), 256, 0, s>>>(g, p32_xs(g), b64, dinv, c0, b32, d, x,
+                                                                  npr, npairs);
   SG_CHECK_LAUNCH();
 }
 
