@@ -302,7 +302,9 @@ def run_gpu(args):
     peak, peak_kind = _peaks()
     b32 = 8 * n_free + 4 * n_elem
     b64 = 16 * n_free + 8 * n_elem
-    bl1 = (243 * 8 + 48) * nn1
+    # level-1 SpMV on the symmetric stencil copy (126 of 243 coefficients per
+    # node from HBM; SG_ST64_FULL=1 selects the full 243)
+    bl1 = ((243 if os.environ.get("SG_ST64_FULL") else 126) * 8 + 48) * nn1
     comps["fine_apply_fp32"] = {"ms": t32, "alg_bytes": b32, "gbs": b32 / t32 / 1e6}
     comps["fine_apply_fp64"] = {"ms": t64, "alg_bytes": b64, "gbs": b64 / t64 / 1e6}
     comps["fine_apply_bf16_tcgen05"] = {"ms": tbf, "alg_bytes": b32, "gbs": b32 / tbf / 1e6}

@@ -720,7 +720,11 @@ extern "C" int sg_hier_profile(sg_hier* h, int what, int reps, double* ms_avg, v
         case 2: {
           SG_REQUIRE(H.lv.size() > 1, "no level 1");
           sg::Level& L1 = *H.lv[1];
-          sg::stencil_apply<double>(*L1.g, L1.st.T64.p, L1.w.r.p, L1.w.y64.p, s);
+          if (L1.st.T64s.p)  // the symmetric copy the single-GPU cycle reads
+            sg::stencil_sym64(*L1.g, L1.st.T64s.p, 0, L1.w.r.p, L1.w.y64.p, nullptr, nullptr, nullptr, 0.0,
+                              0.0, true, s);
+          else
+            sg::stencil_apply<double>(*L1.g, L1.st.T64.p, L1.w.r.p, L1.w.y64.p, s);
           break;
         }
         case 3: {

@@ -117,7 +117,10 @@ void level_apply(Hier& H, Level& L, int tag, const void* x, void* y, cudaStream_
     fine_apply_tag(*H.fine, tag, x, y, s);
     return;
   }
-  if (tag == TAG_FP64) {
+  if (tag == TAG_FP64 && L.st.T64s.p && !H.comm) {
+    stencil_sym64(*L.g, L.st.T64s.p, 0, (const double*)x, (double*)y, nullptr, nullptr, nullptr, 0.0, 0.0,
+                  true, s);
+  } else if (tag == TAG_FP64) {
     stencil_apply<double>(*L.g, L.st.T64.p, (const double*)x, (double*)y, s);
   } else if (tag == TAG_FP32) {
     SG_REQUIRE(L.st.T32.p, "fp32 operator copy missing");
@@ -270,6 +273,22 @@ static void smooth_p32(Hier& H, Level& L, const double* b64, const double* x0, d
   if (!out_done) from_p32<double>(g, x, out, s);
 }
 
+// fused FP64 stencil Chebyshev step / residual on the symmetric copy when
+// the level has one (single GPU), else on the full stencil
+static void cheb64(Level& L, const double* x, double* xout, const double* b, double* d, double A,
+                   double AC, bool first, cudaStream_t s) {
+  if (L.st.T64s.p)
+    stencil_sym64(*L.g, L.st.T64s.p, 1, x, xout, b, L.dinv.p, d, A, AC, first, s);
+  else
+    stencil_cheb64(*L.g, L.st.T64.p, x, xout, b, L.dinv.p, d, A, AC, first, s);
+}
+static void res64(Level& L, const double* x, const double* r, double* out, cudaStream_t s) {
+  if (L.st.T64s.p)
+    stencil_sym64(*L.g, L.st.T64s.p, 2, x, out, r, nullptr, nullptr, 0.0, 0.0, true, s);
+  else
+    stencil_res64(*L.g, L.st.T64.p, x, r, out, s);
+}
+
 // FP64 Galerkin level, Chebyshev: every apply fused with its update
 // (stencil_cheb64); iterates alternate between `out` and the y64 scratch so
 // the last lands in `out` and no step reads the buffer it writes.
@@ -292,14 +311,14 @@ static bool smooth_st64(Hier& H, Level& L, const double* b, const double* x0, do
     launch_ew(n, s, [&](int nb, int nt) { cheb_first0_kernel<double><<<nb, nt, 0, s>>>(n, L.dinv.p, b, c0, d, x1); });
     cur = x1;
   } else {
-    stencil_cheb64(*L.g, L.st.T64.p, x0, buf(1), b, L.dinv.p, d, c0, 0.0, true, s);
+    cheb64(L, x0, buf(1), b, d, c0, 0.0, true, s);
     cur = buf(1);
   }
   double a = 2.0 / sigma;
   for (int it = 1; it < D; ++it) {
     const double c = delta * delta * a / 4.0;
     a = 1.0 / (sigma - c);
-    stencil_cheb64(*L.g, L.st.T64.p, cur, buf(it + 1), b, L.dinv.p, d, a, a * c, false, s);
+    cheb64(L, cur, buf(it + 1), b, d, a, a * c, false, s);
     cur = buf(it + 1);
   }
   if (D < 1) launch_ew(n, s, [&](int nb, int nt) { copy_kernel<<<nb, nt, 0, s>>>(n, x0, out); });
@@ -340,7 +359,7 @@ void cycle(Hier& H, int l, int gamma, cudaStream_t s) {
   level_smooth(H, l, L.w.r.p, nullptr, x64, s);
   for (int g = 0; g < gamma; ++g) {
     if (L.tag == TAG_FP64 && !L.is_fine && !H.comm && !std::getenv("SG_ST64_UNFUSED")) {
-      stencil_res64(*L.g, L.st.T64.p, x64, L.w.r.p, L.w.x.p, s);  // r - A x in one pass
+      res64(L, x64, L.w.r.p, L.w.x.p, s);  // r - A x in one pass
     } else if (L.tag == TAG_FP64) {
       level_apply(H, L, TAG_FP64, x64, L.w.y64.p, s);
       launch_ew(n, s, [&](int nb, int nt) { residual_kernel<double><<<nb, nt, 0, s>>>(n, L.w.r.p, L.w.y64.p, L.w.x.p); });
@@ -572,6 +591,9 @@ std::unique_ptr<Hier> hier_build(FineOp* fine, FineWork& fw, const HParams& p, c
         stencil_tile<float>(*L.g, L.st.A32.p, L.st.T32, s);
       }
       stencil_tile<double>(*L.g, L.st.A64.p, L.st.T64, s);
+      // single-GPU FP64 smoothing / residual / apply read the symmetric copy
+      // (SG_ST64_FULL=1: the full stencil, bit-exact to the reference SpMV)
+      if (L.tag == TAG_FP64 && !std::getenv("SG_ST64_FULL")) stencil_sym_tile(*L.g, L.st.A64.p, L.st.T64s, s);
     }
     launch_ew(int64_t(n), s, [&](int nb, int nt) { recip_kernel<<<nb, nt, 0, s>>>(int64_t(n), L.diag.p, L.dinv.p, L.dinv32.p); });
     L.p32 = L.is_fine && L.tag == TAG_FP32 && p32_supported(*fine) && !std::getenv("SG_NO_P32");

@@ -67,6 +67,12 @@ int kKwRowHost(int q);
 // fused FP64 stencil apply + Chebyshev step / residual (sg_stencil.cu)
 void stencil_cheb64(const Grid& g, const double* At, const double* x, double* xout, const double* b,
                     const double* dinv, double* d, double A, double AC, bool first, cudaStream_t s);
+// Symmetric (upper-slot) FP64 stencil copy and its SpMV (sg_stencil.cu):
+// mode 0 y = A x, 1 fused Chebyshev step (as stencil_cheb64), 2 r - A x.
+void stencil_sym_tile(const Grid& g, const double* A, DBuf<double>& Ts, cudaStream_t s);
+void stencil_sym64(const Grid& g, const double* Ts, int mode, const double* x, double* out,
+                   const double* b, const double* dinv, double* d, double A, double AC, bool first,
+                   cudaStream_t s);
 void stencil_res64(const Grid& g, const double* At, const double* x, const double* r, double* out,
                    cudaStream_t s);
 int kKwColHost(int q);
@@ -112,6 +118,7 @@ struct Stencil {
   DBuf<double> A64;
   DBuf<float> A32;
   DBuf<double> T64;  // tiled copies for the SpMV (stencil_tile)
+  DBuf<double> T64s;  // symmetric tiled copy (stencil_sym_tile), single-GPU FP64 levels
   DBuf<float> T32;
   int64_t nnz = 0;  // nonzero entries on free rows (CSR nnz of the reference)
 };

@@ -126,6 +126,112 @@ __global__ void __launch_bounds__(128) stencil_fused_kernel(GridDesc g, const do
   }
 }
 
+// ---------------------------------------------------------------------------
+// Symmetric ("upper") copy of an FP64 Galerkin stencil: only the diagonal
+// slot 13 and the 13 lexicographically later slots 14..26 are stored (126
+// of 243 coefficients per node, tiled like stencil_tile); a row's lower
+// slot s < 13 uses the transpose of the block node j = i + off(s) stores in
+// its mirror slot 26 - s.  The Galerkin operators are symmetric to rounding
+// (P^T K P, K symmetric; the reference's assembled bits differ from exact
+// symmetry by ~1 ulp), so y agrees with the full-stencil SpMV to ~1e-16
+// relative while the operator streams 1008 instead of 1944 bytes per node
+// from HBM -- the L1 smoother passes are HBM-bound at 92% of the roofline.
+// Every row still sums its 27 blocks in the ascending-column (csr_matvec)
+// order; deterministic.
+constexpr int kSymQ = 126;
+__global__ void stencil_sym_tile_kernel(int64_t nn, int64_t ntiles, const double* __restrict__ A,
+                                        double* __restrict__ Ts) {
+  const int64_t idx = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (idx >= ntiles * kSymQ * 32) return;
+  const int64_t lane = idx & 31, q = (idx >> 5) % kSymQ, tile = (idx >> 5) / kSymQ;
+  const int64_t node = tile * 32 + lane;
+  Ts[idx] = node < nn ? A[(13 * 9 + q) * nn + node] : 0.0;
+}
+void stencil_sym_tile(const Grid& g, const double* A, DBuf<double>& Ts, cudaStream_t s) {
+  const int64_t nn = g.d.nnodes(), nt = (nn + 31) / 32;
+  Ts.alloc(size_t(nt * kSymQ * 32));
+  stencil_sym_tile_kernel<<<grid_blocks(nt * kSymQ * 32, 256), 256, 0, s>>>(nn, nt, A, Ts.p);
+  SG_CHECK_LAUNCH();
+}
+
+// mode 0: y = A x; mode 1: Chebyshev step (stencil_fused_kernel mode 1);
+// mode 2: out = rr - A x.  Same epilogue operations as the full-stencil kernels.
+__global__ void __launch_bounds__(128) stencil_sym_kernel(GridDesc g, const double* __restrict__ Ts,
+                                                          const double* __restrict__ x, int mode,
+                                                          const double* __restrict__ b,
+                                                          const double* __restrict__ dinv,
+                                                          double* __restrict__ d, double* __restrict__ xout,
+                                                          double A, double AC, int first) {
+  const int64_t nn = g.nnodes();
+  const int64_t node = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (node >= nn) return;
+  const int NX = g.nx + 1, NY = g.ny + 1;
+  const int64_t NXY = int64_t(NX) * NY;
+  const int nd32 = int(node), jk = nd32 / NX;
+  const int i = nd32 - jk * NX, j = jk % NY, k = jk / NY;
+  const int64_t oi[3] = {i > 0 ? -1 : 0, 0, i < g.nx ? 1 : 0};
+  const int64_t oj[3] = {j > 0 ? -NX : 0, 0, j < g.ny ? NX : 0};
+  const int64_t ok[3] = {k > 0 ? -NXY : 0, 0, k < g.nz ? NXY : 0};
+  const bool in_i[3] = {i > 0, true, i < g.nx};
+  const bool in_j[3] = {j > 0, true, j < g.ny};
+  const bool in_k[3] = {k > 0, true, k < g.nz};
+  double s[3] = {0.0, 0.0, 0.0}, xc[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+  for (int slot = 0; slot < 27; ++slot) {
+    const int64_t nb = node + oi[slot % 3] + oj[(slot / 3) % 3] + ok[slot / 9];
+    const double x0 = x[3 * nb], x1 = x[3 * nb + 1], x2 = x[3 * nb + 2];
+    if (slot == 13) {
+      xc[0] = x0;
+      xc[1] = x1;
+      xc[2] = x2;
+    }
+    double a[9];
+    if (slot >= 13) {
+      const double* p = Ts + (node >> 5) * (kSymQ * 32) + (slot - 13) * (9 * 32) + (node & 31);
+#pragma unroll
+      for (int e = 0; e < 9; ++e) a[e] = __ldcs(p + e * 32);
+    } else {
+      // transpose of the neighbour's mirror block (zero outside the grid,
+      // where nb is clamped onto the node itself)
+      const bool in = in_i[slot % 3] && in_j[(slot / 3) % 3] && in_k[slot / 9];
+      const double* p = Ts + (nb >> 5) * (kSymQ * 32) + (13 - slot) * (9 * 32) + (nb & 31);
+#pragma unroll
+      for (int ra = 0; ra < 3; ++ra)
+#pragma unroll
+        for (int cb = 0; cb < 3; ++cb) a[ra * 3 + cb] = in ? __ldg(p + (cb * 3 + ra) * 32) : 0.0;
+    }
+#pragma unroll
+    for (int r = 0; r < 3; ++r) {
+      s[r] = __dadd_rn(s[r], __dmul_rn(a[3 * r + 0], x0));
+      s[r] = __dadd_rn(s[r], __dmul_rn(a[3 * r + 1], x1));
+      s[r] = __dadd_rn(s[r], __dmul_rn(a[3 * r + 2], x2));
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < 3; ++r) {
+    const int64_t q = 3 * node + r;
+    if (mode == 0) {
+      xout[q] = s[r];
+    } else if (mode == 2) {
+      xout[q] = __dsub_rn(b[q], s[r]);
+    } else {
+      const double rv = __dsub_rn(b[q], s[r]);
+      double dv = __dmul_rn(A, __dmul_rn(dinv[q], rv));
+      if (!first) dv = __dadd_rn(dv, __dmul_rn(AC, d[q]));
+      d[q] = dv;
+      xout[q] = __dadd_rn(xc[r], dv);
+    }
+  }
+}
+void stencil_sym64(const Grid& g, const double* Ts, int mode, const double* x, double* out,
+                   const double* b, const double* dinv, double* d, double A, double AC, bool first,
+                   cudaStream_t s) {
+  const int64_t nn = g.d.nnodes();
+  stencil_sym_kernel<<<grid_blocks(nn, 128), 128, 0, s>>>(g.d, Ts, x, mode, b, dinv, d, out, A, AC,
+                                                          first ? 1 : 0);
+  SG_CHECK_LAUNCH();
+}
+
 void stencil_cheb64(const Grid& g, const double* At, const double* x, double* xout, const double* b,
                     const double* dinv, double* d, double A, double AC, bool first, cudaStream_t s) {
   const int64_t nn = g.d.nnodes();
