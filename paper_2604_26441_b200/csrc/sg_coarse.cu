@@ -3,12 +3,13 @@
 //  * pcg80: the reference's fixed-count Jacobi-PCG on K + eps*I
 //    (_fixed_jacobi_pcg, hierarchy.py:139-162) as ONE persistent cooperative
 //    kernel (one block per SM): the 80 dependent steps never return to the
-//    host.  Each block keeps its operator rows resident in shared memory for
-//    the whole solve; per step: phase A (q = (K+eps I) p with p = z + beta
+//    host.  The contiguous-range kernel below keeps its operator rows in
+//    shared memory; per step: phase A (q = (K+eps I) p with p = z + beta
 //    p_old recomputed for the neighbours on the fly, branch-free), a grid
 //    all-reduce (counter barrier + every block summing the block partials in
 //    index order: deterministic), phase B (x, r, z updates) and a second
-//    all-reduce.
+//    all-reduce.  The default is the brick-partitioned pipelined kernel
+//    (pcg80_brick_kernel<2>) further down, with its rows in tensor memory.
 //  * dense: Cholesky of K + eps*I computed on device at setup, then the
 //    explicit inverse, so each V-cycle's coarsest solve is one GEMV.
 #include <cmath>
@@ -236,9 +237,11 @@ __global__ void __launch_bounds__(kPcgThreads) pcg80_kernel(Pcg80Args P) {
 // ------------------------------------------------------------ brick pcg80
 // Same algorithm, data-parallel over 3D node bricks (one brick per block,
 // one block per SM) instead of contiguous node ranges:
-//  * the operator rows stay on chip for all steps: the dj = -1 stencil row of
-//    each thread's dk plane in registers (27 doubles), the other 18 slots in
-//    shared memory (the full operator does not fit in 227 KB);
+//  * the operator rows stay on chip for all steps: variants 0/1 keep the
+//    dj = -1 stencil row of each thread's dk plane in registers (27 doubles)
+//    and the other 18 slots in shared memory (the full operator does not fit
+//    in 227 KB); the pipelined variant 2 keeps 7 of its 9 rows in tensor
+//    memory and 2 in shared memory (kBrTmRows);
 //  * p lives in shared memory on the brick plus a one-node halo and is
 //    updated there, p = z + beta p, for halo nodes too (the same expression
 //    on the same bits as the owner's), so z is the only vector that crosses
