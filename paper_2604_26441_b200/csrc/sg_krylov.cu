@@ -21,7 +21,8 @@ enum Slot { S_NB = 0, S_PQ, S_RZ, S_RR, S_OK, S_RZN, S_TR, S_BETA, S_TMP, S_H0 =
 struct Dot {
   const double* a;
   const double* b;
-  __device__ void operator()(int64_t i, double (&acc)[1]) const { acc[0] += a[i] * b[i]; }
+  // explicit fma: the fused kernels below must round exactly like this
+  __device__ void operator()(int64_t i, double (&acc)[1]) const { acc[0] = fma(a[i], b[i], acc[0]); }
 };
 struct DiffSq {  // ||b - t||^2
   const double* b;
@@ -56,7 +57,7 @@ struct PcgStep {  // x += a p; r -= a q; rr
       rv = __dsub_rn(rv, __dmul_rn(c.a, v.q));
       r[i] = rv;
     }
-    acc[0] += rv * rv;
+    acc[0] = fma(rv, rv, acc[0]);
   }
 };
 struct PcgStepPost {
@@ -123,6 +124,115 @@ __global__ void f32_to_f64_k(int64_t n, const float* __restrict__ a, double* __r
 
 inline int nb256(int64_t n) { return grid_blocks(n, 256); }
 
+// ---------------------------------------------------------------------------
+// One GPU: the PCG's reduce-then-update pairs as single cooperative launches.
+//  * pq_step: p.q (krylov.py:137), then x += a p, r -= a q and ||r||^2
+//    (:138-146) -- p and q are re-read from L2 by the second phase;
+//  * rz_pupd: r.z and beta (:158-163), then p = z + beta p (:164).
+// Phase 1 and the cross-block sum are exactly reduce_kernel's (same grid,
+// same per-thread order, same block tree, partials summed in block order --
+// here by every block after a grid barrier instead of by the last block), so
+// the results are bit-identical to the separate launches (and to the slab
+// path with one rank).  Cooperative launch guarantees co-residency.
+__device__ __forceinline__ void grid_barrier(unsigned long long* ctr) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const unsigned long long nb = gridDim.x;
+    const unsigned long long old = atomicAdd(ctr, 1ull);
+    const unsigned long long target = (old / nb + 1) * nb;  // counter grows by nb per launch
+    while (*(volatile unsigned long long*)ctr < target) __nanosleep(32);
+    __threadfence();
+  }
+  __syncthreads();
+}
+// every block: the reduce_kernel last-block sum of partials[0..gridDim)
+__device__ __forceinline__ double sum_partials(const double* partials, double* smem, double* bc) {
+  double tot[1] = {0.0};
+  for (int b = threadIdx.x; b < int(gridDim.x); b += kRedThreads) tot[0] += ((volatile double*)partials)[b];
+  __syncthreads();
+  block_sum<1>(tot, smem);
+  if (threadIdx.x == 0) *bc = tot[0];
+  __syncthreads();
+  return *bc;
+}
+
+__global__ void __launch_bounds__(kRedThreads, 8) pq_step_kernel(int64_t n, double* __restrict__ x,
+                                                              double* __restrict__ r,
+                                                              const double* __restrict__ p,
+                                                              const double* __restrict__ q, double* sc,
+                                                              double* partials, unsigned* counter,
+                                                              unsigned long long* bar) {
+  __shared__ double smem[8];
+  __shared__ double bc;
+  __shared__ bool last;
+  const int64_t stride = int64_t(gridDim.x) * kRedThreads;
+  const int64_t i0 = int64_t(blockIdx.x) * kRedThreads + threadIdx.x;
+  double acc[1] = {0.0};
+  for (int64_t i = i0; i < n; i += stride) acc[0] = fma(p[i], q[i], acc[0]);  // Dot
+  block_sum<1>(acc, smem);
+  if (threadIdx.x == 0) partials[blockIdx.x] = acc[0];
+  const double rz = sc[S_RZ];
+  grid_barrier(bar);
+  const double pq = sum_partials(partials, smem, &bc);
+  if (blockIdx.x == 0 && threadIdx.x == 0) sc[S_PQ] = pq;  // StoreTo
+  // PcgStep with this step length (PcgStep::prep / load / use)
+  const bool ok = isfinite(pq) && pq != 0.0 && isfinite(rz);
+  const double a = ok ? __ddiv_rn(rz, pq) : 0.0;
+  // (same accumulation order as PcgStep's four-deep load batches: sequential in i)
+  double acc2[1] = {0.0};
+  for (int64_t i = i0; i < n; i += stride) {
+    double rn = r[i];
+    if (ok) {
+      x[i] = __dadd_rn(x[i], __dmul_rn(a, p[i]));
+      rn = __dsub_rn(rn, __dmul_rn(a, q[i]));
+      r[i] = rn;
+    }
+    acc2[0] = fma(rn, rn, acc2[0]);
+  }
+  block_sum<1>(acc2, smem);
+  double* part2 = partials + gridDim.x;  // phase-1 partials may still be being read
+  if (threadIdx.x == 0) {
+    part2[blockIdx.x] = acc2[0];
+    __threadfence();
+    last = atomicAdd(counter, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  const double rr = sum_partials(part2, smem, &bc);
+  if (threadIdx.x == 0) {  // PcgStepPost, from the values in registers
+    sc[S_OK] = ok ? 1.0 : 0.0;
+    sc[S_RR] = rr;
+    *counter = 0u;
+  }
+}
+
+__global__ void __launch_bounds__(kRedThreads, 8) rz_pupd_kernel(int64_t n, int64_t nd,
+                                                              const double* __restrict__ r,
+                                                              const double* __restrict__ z,
+                                                              double* __restrict__ p, double* sc,
+                                                              double* partials, unsigned long long* bar) {
+  __shared__ double smem[8];
+  __shared__ double bc;
+  const int64_t stride = int64_t(gridDim.x) * kRedThreads;
+  const int64_t i0 = int64_t(blockIdx.x) * kRedThreads + threadIdx.x;
+  double acc[1] = {0.0};
+  for (int64_t i = i0; i < n; i += stride) acc[0] = fma(r[i], z[i], acc[0]);  // Dot
+  block_sum<1>(acc, smem);
+  if (threadIdx.x == 0) partials[blockIdx.x] = acc[0];
+  const double rz_old = sc[S_RZ];  // read by every block before block 0 replaces it
+  grid_barrier(bar);
+  const double t = sum_partials(partials, smem, &bc);
+  const double beta = __ddiv_rn(t, rz_old);  // RznPost
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    sc[S_RZN] = t;
+    sc[S_BETA] = beta;
+    sc[S_RZ] = t;
+  }
+  for (int64_t i = i0; i < nd; i += stride) p[i] = __dadd_rn(z[i], __dmul_rn(beta, p[i]));  // pupd
+}
+
 struct View {  // non-owning handle on a reused SolverWork buffer
   double* p;
 };
@@ -171,6 +281,38 @@ struct Ctx {
       f32_to_f64_k<<<nb256(nd), 256, 0, s>>>(nd, t32b.p, y);
       SG_CHECK_LAUNCH();
     }
+  }
+  // fused cooperative reduce-then-update kernels (one GPU); 0 = unavailable
+  int fused_blocks() {
+    static int per_sm = -1;
+    if (sys.dist || std::getenv("SG_PCG_UNFUSED")) return 0;
+    if (per_sm < 0) {
+      int a = 0, b = 0;
+      SG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a, pq_step_kernel, kRedThreads, 0));
+      SG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, rz_pupd_kernel, kRedThreads, 0));
+      per_sm = std::min(a, b);
+    }
+    const int nb = red_blocks(nown);
+    return nb <= per_sm * kNumSMs ? nb : 0;
+  }
+  void pq_step(double* x, double* r, const double* p, const double* q, int nb) {
+    int64_t n = nown;
+    double* scp = sc.p;
+    double* part = red.partials.p;
+    unsigned* cnt = red.counter.p;
+    unsigned long long* bar = red.gbar.p;
+    void* args[] = {&n, &x, &r, &p, &q, &scp, &part, &cnt, &bar};
+    SG_CUDA(cudaLaunchCooperativeKernel((const void*)pq_step_kernel, dim3(nb), dim3(kRedThreads), args, 0, s));
+    SG_CHECK_LAUNCH();
+  }
+  void rz_pupd(const double* r, const double* z, double* p, int nb) {
+    int64_t n = nown, ndd = nd;
+    double* scp = sc.p;
+    double* part = red.partials.p;
+    unsigned long long* bar = red.gbar.p;
+    void* args[] = {&n, &ndd, &r, &z, &p, &scp, &part, &bar};
+    SG_CUDA(cudaLaunchCooperativeKernel((const void*)rz_pupd_kernel, dim3(nb), dim3(kRedThreads), args, 0, s));
+    SG_CHECK_LAUNCH();
   }
   // z = apply_M(r)
   void M(const double* r, double* z) {
@@ -266,8 +408,12 @@ void pcg_native(NativeSys& sys, const double* b, double* x, const SolverCfg& cfg
   int kind = 1;  // cap
   for (int it = 0; it < cfg.maxiter; ++it) {
     C.K(p.p, q.p);
-    C.dot(p.p, q.p, S_PQ);
-    C.reduce(PcgStep{x + C.off, r + C.off, p.p + C.off, q.p + C.off, C.sc.p}, PcgStepPost{C.sc.p}, S_TMP);
+    if (const int fb = C.fused_blocks()) {
+      C.pq_step(x, r, p.p, q.p, fb);
+    } else {
+      C.dot(p.p, q.p, S_PQ);
+      C.reduce(PcgStep{x + C.off, r + C.off, p.p + C.off, q.p + C.off, C.sc.p}, PcgStepPost{C.sc.p}, S_TMP);
+    }
     double h[4];
     SG_CUDA(cudaMemcpyAsync(h, C.sc.p + S_PQ, 4 * sizeof(double), cudaMemcpyDeviceToHost, s));
     SG_CUDA(cudaStreamSynchronize(s));
@@ -295,9 +441,13 @@ void pcg_native(NativeSys& sys, const double* b, double* x, const SolverCfg& cfg
       target *= 0.1;
     }
     C.M(r, z.p);
-    C.reduce(Dot{r + C.off, z.p + C.off}, RznPost{C.sc.p}, S_TMP);
-    pupd_kernel<<<nb256(nd), 256, 0, s>>>(nd, z.p, p.p, C.sc.p);
-    SG_CHECK_LAUNCH();
+    if (const int fb = C.fused_blocks()) {
+      C.rz_pupd(r, z.p, p.p, fb);
+    } else {
+      C.reduce(Dot{r + C.off, z.p + C.off}, RznPost{C.sc.p}, S_TMP);
+      pupd_kernel<<<nb256(nd), 256, 0, s>>>(nd, z.p, p.p, C.sc.p);
+      SG_CHECK_LAUNCH();
+    }
   }
   const double tr = C.true_res(b, x, q.p, normb);
   out.converged = std::isfinite(tr) && tr < cfg.tol;

@@ -24,11 +24,14 @@ inline int red_blocks(int64_t n) {
 struct RedWork {
   DBuf<double> partials;  // kRedMaxBlocks * 8
   DBuf<unsigned> counter;
+  DBuf<unsigned long long> gbar;  // grid barrier of the fused PCG kernels (monotonic)
   void init(cudaStream_t s) {
     if (!partials.p) {
       partials.alloc(size_t(kRedMaxBlocks) * 8);
       counter.alloc(1);
       counter.zero(s);
+      gbar.alloc(1);
+      gbar.zero(s);
     }
   }
 };

@@ -367,3 +367,37 @@ def test_symmetric_stencil_matches_full_stencil():
         else:
             tol = 1e-13 if "l1" in k or "(16, 8, 8)" in k or "(24, 16, 12)" in k else 1e-5
             assert _rel(a, b) < tol, (k, _rel(a, b))
+
+
+def test_fused_pcg_reductions_bit_identical():
+    """One GPU: p.q + the PCG step and r.z + the p update run as two cooperative
+    launches; SG_PCG_UNFUSED=1 runs the separate reduction / update kernels.
+    Same grid, per-thread order and block-order sums: identical histories."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = (
+        "import sys, warnings, numpy as np; sys.path.insert(0, %r)\n"
+        "import paper_2604_26441_b200 as P\n"
+        "out = {}\n"
+        "for dims, kind, pol in (((16,8,8),'binary','fp32'), ((48,24,24),'random_floor','fp32'),"
+        " ((24,12,12),'binary','fp64')):\n"
+        "    g = P.build_cantilever(*dims)\n"
+        "    op = P.FineOperator(g, P.simp_modulus(P.make_state(kind, *dims, vf=0.5, seed=42), 3.0))\n"
+        "    with warnings.catch_warnings():\n"
+        "        warnings.simplefilter('ignore')\n"
+        "        h = P.build_hierarchy(op, 4, pol)\n"
+        "    rep = P.pcg(op.matvec, h.vcycle, g.load[g.free_dofs], P.SolverConfig(tol=1e-8, maxiter=200))\n"
+        "    out[str(dims) + 'h'] = np.array(rep.residual_history)\n"
+        "    out[str(dims) + 'x'] = rep.x\n"
+        "    rj = P.flat_jacobi_pcg(op, g.load[g.free_dofs], P.SolverConfig(tol=1e-6, maxiter=60))\n"
+        "    out[str(dims) + 'j'] = np.array(rj.residual_history)\n"
+        "np.savez(sys.argv[1], **out)\n" % root)
+    res = {}
+    for name, env in (("fused", {}), ("unfused", {"SG_PCG_UNFUSED": "1"})):
+        path = f"/tmp/_pcgf_{name}.npz"
+        subprocess.run([sys.executable, "-c", code, path], check=True, env=dict(os.environ, **env))
+        res[name] = np.load(path)
+    for k in res["fused"].files:
+        assert np.array_equal(res["fused"][k], res["unfused"][k]), k
