@@ -5,5 +5,9 @@ import paper_2604_26441_b200 as P
 dims = tuple(int(v) for v in sys.argv[2].split(","))
 g = P.build_cantilever(*dims)
 op = P.FineOperator(g, P.simp_modulus(P.make_state("random_floor", *dims, vf=0.5, seed=42), 3.0))
-u = P.SplitMix64(3).gaussian(g.n_free).astype(np.float32)
-np.save(sys.argv[1], op.matvec_tagged(u, P.PrecisionTag.FP32))
+tag = sys.argv[3] if len(sys.argv) > 3 else "fp32"
+u = P.SplitMix64(3).gaussian(g.n_free)
+if tag == "fp64":
+    np.save(sys.argv[1], op.matvec(u))
+else:
+    np.save(sys.argv[1], op.matvec_tagged(u.astype(np.float32), P.PrecisionTag.FP32))
