@@ -185,7 +185,7 @@ def _config(args):
             "elements": N ** 3, "levels_requested": 4, "policy": "fp32",
             "parallelism": (f"z-slab partition x{args.gpus} (levels 0-1; NCCL halos + rank-ordered "
                             "dot sums; coarse tail replicated)") if (args.gpus > 1 or args.slab) else "single GPU",
-            "l2": "working set > 126 MB L2 (L1 operator 258 MB); L2 also flushed before each timed solve"}
+            "l2": "working set > 126 MB L2 (level-1 operator 258 MB, its symmetric copy 133 MB); L2 also flushed before each timed solve"}
 
 
 def run_gpu(args):
