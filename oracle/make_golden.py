@@ -175,6 +175,12 @@ BENCH_SPECS = {
                          "ps": (3.0,), "precisions": ("fp64", "fp32", "bf16"),
                          "smoothers": ("chebyshev", "jacobi")},
     "robustness": {"experiment": "robustness", "restart": 50, "maxiter": 500},
+    "sweep_axes": {"experiment": "sweep", "grids": ((8, 4, 4),), "vfs": (0.5,), "ps": (3.0,),
+                   "degrees": (2, 3), "depths": (2, 3), "restarts": (16, 32),
+                   "precisions": ("bf16",)},
+    "solve_jacobi": {"experiment": "solve", "grid": (8, 4, 4), "method": "jacobi", "trials": 1,
+                     "warmups": 0, "state": "binary"},
+    "probe_layered": {"experiment": "probe", "grid": (8, 4, 4), "state": "layered", "p": 4.5},
 }
 
 
