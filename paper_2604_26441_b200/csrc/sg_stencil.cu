@@ -75,7 +75,7 @@ __global__ void __launch_bounds__(128) stencil_apply_kernel(GridDesc g, const T*
 // in sg_hier.cu, so the result is bit-identical to apply-then-update):
 //   mode 1: r = b - Ax; d' = A*(dinv*r) [+ AC*d]; x' = x + d'  (x' != x)
 //   mode 2: out = rr - Ax
-__global__ void __launch_bounds__(128) stencil_fused_kernel(GridDesc g, const double* __restrict__ At,
+__global__ void __launch_bounds__(128, 4) stencil_fused_kernel(GridDesc g, const double* __restrict__ At,
                                                             const double* __restrict__ x, int mode,
                                                             const double* __restrict__ b,
                                                             const double* __restrict__ dinv,
