@@ -35,7 +35,7 @@ __device__ __forceinline__ float add_rn<float>(float a, float b) { return __fadd
 // per apply: memory-level parallelism is the bound).  The summation order is
 // still the scipy csr_matvec order; a 0*x term only adds a signed zero.
 template <class T>
-__global__ void __launch_bounds__(128) stencil_apply_kernel(GridDesc g, const T* __restrict__ At,
+__global__ void __launch_bounds__(128, 4) stencil_apply_kernel(GridDesc g, const T* __restrict__ At,
                                                             const T* __restrict__ x, T* __restrict__ y) {
   const int64_t nn = g.nnodes();
   const int64_t node = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
