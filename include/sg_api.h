@@ -59,7 +59,8 @@ int sg_fine_diagonal(sg_fine* op, double* d_free, void* stream);
 /* FineOperator.assemble_dense (fine_operator.py:88-101): device n_free^2. */
 int sg_fine_dense(sg_fine* op, double* K, void* stream);
 /* Distinct (child << 24 | fixed-local-dof mask) codes of fine elements that
- * touch Dirichlet DOFs (transfer.py:158-164), ascending; host output. */
+ * touch Dirichlet DOFs (transfer.py:158-164), ascending; host output.
+ * codes = NULL: size query (only *n is written). */
 int sg_fine_boundary_codes(sg_fine* op, uint32_t* codes, int cap, int* n);
 
 /* ---------------------------------------------------------------------

@@ -153,6 +153,7 @@ int sg_fine_boundary_codes(sg_fine* f, uint32_t* codes, int cap, int* n) {
     std::vector<uint32_t> c;
     sg::boundary_codes(f->op, c, 0);
     *n = int(c.size());
+    if (codes == nullptr) return;  // size query
     SG_REQUIRE(int(c.size()) <= cap, "boundary code buffer too small");
     std::copy(c.begin(), c.end(), codes);
   });
@@ -755,22 +756,22 @@ extern "C" int sg_hier_profile(sg_hier* h, int what, int reps, double* ms_avg, v
   });
 }
 
-// Development instrumentation: %globaltimer stamps (ns) of block 0 in pcg80
-// step 10 at its phase boundaries (phase A, partial, barrier, total, phase B,
-// partial, barrier, total).  out: 9 int64.
+// Development instrumentation: %globaltimer stamps (ns) of every pcg80 block at
+// its phase boundaries; pipelined brick kernel: steps 8..15, 8 stamps each.
+// out: 64 * 256 int64.
 extern "C" int sg_hier_pcg80_trace(sg_hier* h, long long* out, void* stream) {
   return guard([&] {
     std::lock_guard<std::mutex> lk(h->mu);
     cudaStream_t s = S(stream);
     sg::Hier& H = *h->h;
     SG_REQUIRE(H.coarsest_mode == 1, "coarsest solver is not pcg80");
-    sg::DBuf<long long> t(8 * 256);
+    sg::DBuf<long long> t(64 * 256);
     t.zero(s);
     sg::Level& Lc = *H.lv.back();
     H.pcg.trace = t.p;
     sg::coarsest_solve(H, Lc.w.r.p, Lc.w.x.p, s);
     H.pcg.trace = nullptr;
-    t.download(out, 8 * 256, s);
+    t.download(out, 64 * 256, s);
     SG_CUDA(cudaStreamSynchronize(s));
   });
 }

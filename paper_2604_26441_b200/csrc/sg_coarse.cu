@@ -65,6 +65,16 @@ __device__ __forceinline__ void stamp(long long* tr, int k) {
   }
 }
 
+// Development trace of the brick kernels: stamps k of steps 8..15 of every
+// block, tr[(block * 8 + step - 8) * 8 + k].
+__device__ __forceinline__ void stamp_s(long long* tr, int s, int k) {
+  if (tr && s >= 8 && s < 16 && threadIdx.x == 0) {
+    long long t_;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));
+    tr[(blockIdx.x * 8 + (s - 8)) * 8 + k] = t_;
+  }
+}
+
 // Sum of the per-warp values sm[0..nw) by one warp in a fixed xor tree.
 __device__ __forceinline__ double warp_sum_of(const double* sm, int nw, int lane) {
   double v = lane < nw ? sm[lane] : 0.0;
@@ -292,6 +302,12 @@ __device__ __forceinline__ void ll_store(uint4* a, double v, unsigned flag) {
   asm volatile("st.volatile.global.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(a),
                "r"(unsigned(__double2loint(v))), "r"(flag), "r"(unsigned(__double2hiint(v))),
                "r"(flag) : "memory");
+}
+__device__ __forceinline__ uint4 ll_raw(const uint4* a) {
+  uint4 v;
+  asm volatile("ld.volatile.global.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(a) : "memory");
+  return v;
 }
 __device__ __forceinline__ bool ll_load(const uint4* a, unsigned flag, double& v) {
   unsigned lo, f0, hi, f1;
@@ -770,7 +786,7 @@ __global__ void __launch_bounds__(kBrBlock, 1) pcg80_brick_kernel(BrickArgs P) {
     unsigned epoch = 0;
     double gprev = 0.0, aprev = 0.0;
     for (int s = 0; s < P.steps; ++s) {
-      if (P.trace && s == 10) stamp(P.trace, 0);
+      stamp_s(P.trace, s, 0);
       // m = D^-1 w to the neighbours; (r.u, w.u) published
       double lg = 0.0, ld = 0.0;
       if (act) {
@@ -780,10 +796,10 @@ __global__ void __launch_bounds__(kBrBlock, 1) pcg80_brick_kernel(BrickArgs P) {
       }
       ++epoch;
       br_publish2(lg, ld, P, fbase | epoch, red);
-      if (P.trace && s == 10) stamp(P.trace, 1);
+      stamp_s(P.trace, s, 1);
       fill_ph(unsigned(s) + 1u);
       __syncthreads();
-      if (P.trace && s == 10) stamp(P.trace, 5);
+      stamp_s(P.trace, s, 5);
       // stage every block's partial packets into shared memory while the SpMV
       // runs (cp.async, L2 path); validated and re-polled afterwards
       const unsigned pf = fbase | epoch;
@@ -798,26 +814,51 @@ __global__ void __launch_bounds__(kBrBlock, 1) pcg80_brick_kernel(BrickArgs P) {
           asm volatile("cp.async.commit_group;" ::: "memory");
         }
       });
-      if (P.trace && s == 10) stamp(P.trace, 3);
+      stamp_s(P.trace, s, 3);
       double gam, del;
       if (t < 32) {
         asm volatile("cp.async.wait_all;" ::: "memory");
         __syncwarp();
         double a0[5], a1[5];
+        // staged copies first; every stale packet is then re-polled together
+        // (all loads in flight at once: one L2 round trip per pass)
+        bool ok[10];
 #pragma unroll
         for (int k = 0; k < 5; ++k) {
           const int bb = t + 32 * k;
           a0[k] = 0.0;
           a1[k] = 0.0;
+          ok[2 * k] = ok[2 * k + 1] = true;
           if (bb < nb) {
             const uint4 v0 = pst[bb], v1 = pst[nb + bb];
-            bool ok0 = v0.y == pf && v0.w == pf, ok1 = v1.y == pf && v1.w == pf;
+            ok[2 * k] = v0.y == pf && v0.w == pf;
+            ok[2 * k + 1] = v1.y == pf && v1.w == pf;
             a0[k] = __hiloint2double(int(v0.z), int(v0.x));
             a1[k] = __hiloint2double(int(v1.z), int(v1.x));
-            while (!ok0) ok0 = ll_load(sl + bb, pf, a0[k]);
-            while (!ok1) ok1 = ll_load(sl + nb + bb, pf, a1[k]);
           }
         }
+        bool all = true;
+#pragma unroll
+        for (int k = 0; k < 10; ++k) all = all && ok[k];
+        while (!all) {
+          uint4 v[10];
+#pragma unroll
+          for (int k = 0; k < 10; ++k)
+            if (!ok[k]) v[k] = ll_raw(sl + (k & 1) * nb + t + 32 * (k >> 1));
+          all = true;
+#pragma unroll
+          for (int k = 0; k < 10; ++k) {
+            if (!ok[k]) {
+              ok[k] = v[k].y == pf && v[k].w == pf;
+              if (ok[k]) {
+                const double d = __hiloint2double(int(v[k].z), int(v[k].x));
+                if (k & 1) a1[k >> 1] = d; else a0[k >> 1] = d;
+              }
+            }
+            all = all && ok[k];
+          }
+        }
+        stamp_s(P.trace, s, 6);
         const double r0 = wsum(a0[0] + a0[1] + a0[2] + a0[3] + a0[4]);
         const double r1 = wsum(a1[0] + a1[1] + a1[2] + a1[3] + a1[4]);
         if (t == 0) {
@@ -828,7 +869,7 @@ __global__ void __launch_bounds__(kBrBlock, 1) pcg80_brick_kernel(BrickArgs P) {
       __syncthreads();
       gam = tot2[0];
       del = tot2[1];
-      if (P.trace && s == 10) stamp(P.trace, 2);
+      stamp_s(P.trace, s, 2);
       double beta = 0.0, pap = del;
       if (s > 0) {
         if (!(gam > 0.0) || !isfinite(gam)) break;
@@ -851,6 +892,7 @@ __global__ void __launch_bounds__(kBrBlock, 1) pcg80_brick_kernel(BrickArgs P) {
       }
       gprev = gam;
       aprev = al;
+      stamp_s(P.trace, s, 4);
     }
     if (act) P.x[3 * node + c] = xr;
     if (blockIdx.x == 0 && t == 0) {
@@ -1052,7 +1094,10 @@ void Pcg80::setup(const Grid& g, const double* A, const double* diag, double eps
   SG_CUDA(cudaGetDevice(&dev));
   SG_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
   SG_CUDA(cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
-  bool planned = !getenv("SG_PCG80_RANGE") && brick_plan(g.d, nsm, sx, sy, sz);
+  // the brick kernels' packet flags carry the step in 10 bits (fbase = seq << 10):
+  // longer fixed-step counts run on the contiguous-range kernel
+  bool planned = !getenv("SG_PCG80_RANGE") && 2 * steps_ + 1 < 1024 &&
+                 brick_plan(g.d, nsm, sx, sy, sz);
   if (planned && getenv("SG_BRICK")) {  // development override "sx,sy,sz"
     int a = 0, b = 0, c = 0;
     if (sscanf(getenv("SG_BRICK"), "%d,%d,%d", &a, &b, &c) == 3) { sx = a; sy = b; sz = c; }
@@ -1063,7 +1108,6 @@ void Pcg80::setup(const Grid& g, const double* A, const double* diag, double eps
     smem_bytes = int(sizeof(double)) * (kBrSmemA + 3 * kBrWinMax + kBrOwnVec) +
                  int(sizeof(uint4)) * kBrStage;
     SG_REQUIRE(smem_bytes <= smem_optin, "pcg80 brick kernel shared memory");
-    SG_REQUIRE(2 * steps_ + 1 < 1024, "pcg80 step count too large for the packet flags");
     // 0: Hestenes-Stiefel (two all-reduces per step), 1: Chronopoulos-Gear,
     // 2: pipelined (the all-reduce hidden behind the SpMV)
     variant = getenv("SG_PCG80_HS") ? 0 : getenv("SG_PCG80_CG") ? 1 : 2;

@@ -42,7 +42,20 @@ extern unsigned long long g_sg_launches;
     if (!(cond)) throw ::sg::Error(msg);                                           \
   } while (0)
 
-constexpr int kNumSMs = 148;
+// SM count of the current device (148 on a full B200; fewer under MIG / MPS
+// SM limits), queried once per device.
+inline int num_sms() {
+  static int cache[64] = {0};
+  int dev = 0;
+  SG_CUDA(cudaGetDevice(&dev));
+  if (dev < 0 || dev >= 64) dev = 0;
+  if (cache[dev] == 0) {
+    int n = 0;
+    SG_CUDA(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev));
+    cache[dev] = n > 0 ? n : 1;
+  }
+  return cache[dev];
+}
 
 // Owning device buffer (cudaMalloc'd, freed on destruction).
 template <class T>

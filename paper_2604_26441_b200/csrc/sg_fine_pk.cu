@@ -465,7 +465,7 @@ static void launch_pk(const FineOp& op, const float* u, float* y, const PkEpi& e
   PkCoef C;
   SG_REQUIRE(op.walsh_ok && pk_params(op, C), "P32 apply: element matrix lacks the Walsh block form");
   const GridDesc& g = op.grid.d;
-  const PkPlan pl = pk_plan(g, kNumSMs);
+  const PkPlan pl = pk_plan(g, num_sms());
   const int P = pl.P, R = pl.R, SX = pl.SX, kchunk = pl.kchunk;
   const int threads = ((P * R + 31) / 32) * 32;
   dim3 grid(pl.T, pl.tilesy, pl.nch);

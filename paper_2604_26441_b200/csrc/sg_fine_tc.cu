@@ -230,7 +230,7 @@ void fine_apply_bf16_tc(const FineOp& op, const float* u, float* y, cudaStream_t
   const int tx = (g.nx + 1 + kTX - 2) / (kTX - 1);
   const int ty = (g.ny + 1 + kTY - 2) / (kTY - 1);
   const int planes = g.nz + 1;
-  int nchunk = std::max(1, std::min((2 * kNumSMs + tx * ty - 1) / (tx * ty), (planes + 3) / 4));
+  int nchunk = std::max(1, std::min((2 * num_sms() + tx * ty - 1) / (tx * ty), (planes + 3) / 4));
   const int kchunk = (planes + nchunk - 1) / nchunk;
   nchunk = (planes + kchunk - 1) / kchunk;
   dim3 grid(tx, ty, nchunk);

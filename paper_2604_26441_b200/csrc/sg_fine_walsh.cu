@@ -243,8 +243,8 @@ static void launch_walsh(const FineOp& op, const T* u, T* y, const T* E, const K
     const int kc = (planes + nc - 1) / nc;
     const int n = (planes + kc - 1) / kc;
     const int ctas = tx * ty * n;
-    const int waves = (ctas + 2 * kNumSMs - 1) / (2 * kNumSMs);
-    const int per_sm = (ctas + kNumSMs - 1) / kNumSMs;
+    const int waves = (ctas + 2 * num_sms() - 1) / (2 * num_sms());
+    const int per_sm = (ctas + num_sms() - 1) / num_sms();
     const int cost = std::max(per_sm, 2 * waves) * (kc + 1);
     if (cost < best_cost) { best_cost = cost; best = n; }
   }

@@ -293,7 +293,7 @@ struct Ctx {
       per_sm = std::min(a, b);
     }
     const int nb = red_blocks(nown);
-    return nb <= per_sm * kNumSMs ? nb : 0;
+    return nb <= per_sm * num_sms() ? nb : 0;
   }
   void pq_step(double* x, double* r, const double* p, const double* q, int nb) {
     int64_t n = nown;
@@ -447,6 +447,14 @@ void pcg_native(NativeSys& sys, const double* b, double* x, const SolverCfg& cfg
       C.reduce(Dot{r + C.off, z.p + C.off}, RznPost{C.sc.p}, S_TMP);
       pupd_kernel<<<nb256(nd), 256, 0, s>>>(nd, z.p, p.p, C.sc.p);
       SG_CHECK_LAUNCH();
+    }
+    if (it + 1 == cfg.maxiter) {
+      // the loop-top check of r.z (krylov.py:160-162) has no next iteration
+      // here: a non-finite r.z on the last allowed iteration is non_finite
+      double rzn = 0.0;
+      SG_CUDA(cudaMemcpyAsync(&rzn, C.sc.p + S_RZ, sizeof(double), cudaMemcpyDeviceToHost, s));
+      SG_CUDA(cudaStreamSynchronize(s));
+      if (!std::isfinite(rzn)) kind = 3;
     }
   }
   const double tr = C.true_res(b, x, q.p, normb);

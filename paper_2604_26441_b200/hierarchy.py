@@ -263,9 +263,12 @@ def build_hierarchy(op: FineOperator, levels: int = 4, policy: str = "fp32",
             cached = np.array([lev.lam_max for lev in lambda_cache.levels], dtype=np.float64)
     coarse_cfg = SmootherConfig(smoother.kind, coarse_smooth_steps, smoother.alpha, smoother.omega)
     lib = _native.load()
-    cap = 4096
-    codes = np.zeros(cap, dtype=np.uint32)
+    # size query first (codes = NULL): user Dirichlet masks can produce any
+    # number of distinct (child, local-mask) codes
     ncodes = ctypes.c_int()
+    _native.check(lib.sg_fine_boundary_codes(op.handle, None, 0, ctypes.byref(ncodes)))
+    cap = max(1, ncodes.value)
+    codes = np.zeros(cap, dtype=np.uint32)
     _native.check(lib.sg_fine_boundary_codes(op.handle, codes.ctypes.data, cap,
                                              ctypes.byref(ncodes)))
     codes = codes[: ncodes.value]

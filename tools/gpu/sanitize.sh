@@ -1,0 +1,22 @@
+# compute-sanitizer over the -m gpu parity suite (memcheck) and the kernels
+# with shared-memory / cross-block protocols (racecheck, synccheck).
+# Summaries -> gpurun_out/sanitize_<tool>.txt
+CS=/usr/local/cuda/bin/compute-sanitizer
+SEL_ALL="tests/test_gpu_parity.py tests/test_reference_behaviour_gpu.py"
+DESEL="not 100cube and not packed_tiling and not symmetric_stencil and not fused_pcg and not fused_smoothers"
+SEL_SYNC="fine_apply_all_tags or pcg80 or hierarchy_and_cycle or outer_solver or galerkin_levels or transfers"
+for tool in memcheck racecheck synccheck initcheck; do
+  if [ $tool = memcheck ]; then K="$DESEL"; else K="($SEL_SYNC) and ($DESEL)"; fi
+  timeout 1500 $CS --tool $tool --target-processes all --print-limit 30 --error-exitcode 0 \
+      python -m pytest $SEL_ALL -m gpu -q -x -k "$K" -p no:cacheprovider \
+      > gpurun_out/sanitize_$tool.txt 2>&1
+  echo "$tool rc=$?" >> gpurun_out/sanitize_rc.txt
+done
+# synccheck reports "Barrier error ... Missing init" at shared address 0 in the
+# TMEM-resident pipelined pcg80 kernel (no mbarrier in that kernel: the
+# tcgen05.alloc result slot); re-run the same test on the variants without TMEM
+for v in SG_PCG80_HS SG_PCG80_CG; do
+  env $v=1 timeout 900 $CS --tool synccheck --print-limit 5 --error-exitcode 0 \
+      python -m pytest tests/test_gpu_parity.py -m gpu -q -x -k "pcg80_and_dense or pcg80_brick_vs" \
+      -p no:cacheprovider > gpurun_out/sanitize_synccheck_$v.txt 2>&1
+done

@@ -1,0 +1,35 @@
+"""Development aid: per-phase timing of pcg80 steps 8..15 for every block of the
+pipelined brick kernel (%globaltimer stamps; sg_hier_pcg80_trace).
+stamps: 0 step start, 1 published (m + partials), 5 halo filled, 3 SpMV done,
+6 partial packets validated (warp 0), 2 (gamma, delta) known, 4 update done."""
+import sys, warnings
+sys.path.insert(0, ".")
+import numpy as np
+import paper_2604_26441_b200 as P
+from paper_2604_26441_b200 import _dev, _native
+lib = _native.load()
+N = int(sys.argv[1]) if len(sys.argv) > 1 else 100
+g = P.build_cantilever(N, N, N)
+op = P.FineOperator(g, P.simp_modulus(P.make_state("uniform", N, N, N, vf=0.5), 3.0))
+with warnings.catch_warnings():
+    warnings.simplefilter("ignore")
+    h = P.build_hierarchy(op, 4, "fp32")
+h.vcycle(np.ones(g.n_free))
+NAMES = [(0, "start"), (1, "publish"), (5, "fill"), (3, "spmv"), (6, "validate"), (2, "collect"), (4, "update")]
+for rep in range(2):
+    t = np.zeros(64 * 256, dtype=np.int64)
+    _native.check(lib.sg_hier_pcg80_trace(h._hh, t.ctypes.data, _dev.stream()))
+    t = t.reshape(256, 8, 8)
+    nb = int((t[:, 0, 0] > 0).sum())
+    t = t[:nb].astype(np.float64) / 1e3  # us
+    starts = t[:, :, 0]
+    period = np.diff(starts, axis=1)  # block x 7
+    print(f"rep {rep}: blocks {nb}; step period med {np.median(period):.3f} us "
+          f"(min {period.min():.3f} max {period.max():.3f}); start skew per step "
+          + " ".join(f"{v:.2f}" for v in (starts.max(0) - starts.min(0))))
+    prev = 0
+    for k, name in NAMES[1:]:
+        d = t[:, :, k] - t[:, :, prev]
+        print(f"  {name:9s} med {np.median(d):6.3f}  p90 {np.percentile(d, 90):6.3f}  max {d.max():6.3f} us")
+        prev = k
+    # global step boundary: first block start to last block start of next step
