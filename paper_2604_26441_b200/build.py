@@ -26,6 +26,8 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-std=c++17", "-O3", "-lineinfo", "--expt-relaxed-constexpr",
          "-Xcompiler", "-fPIC,-ffp-contract=off", "-I", INCLUDE]
+# development aid only (e.g. -DSG_TRACE_CLOCK for cycle-resolution pcg80 traces)
+FLAGS += os.environ.get("SG_NVCC_EXTRA", "").split()
 
 
 def _sources():

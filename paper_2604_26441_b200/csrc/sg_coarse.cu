@@ -15,6 +15,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <type_traits>
 #include "sg_coarse.cuh"
 
 namespace sg {
@@ -70,7 +71,11 @@ __device__ __forceinline__ void stamp(long long* tr, int k) {
 __device__ __forceinline__ void stamp_s(long long* tr, int s, int k) {
   if (tr && s >= 8 && s < 16 && threadIdx.x == 0) {
     long long t_;
+#ifdef SG_TRACE_CLOCK
+    t_ = clock64();  // SM cycles: fine-grained within a block, not comparable across SMs
+#else
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));
+#endif
     tr[(blockIdx.x * 8 + (s - 8)) * 8 + k] = t_;
   }
 }
@@ -272,7 +277,6 @@ constexpr int kBrLn = kBrCap + (kBrBlock - kBrThreads);  // row pitch of the per
 constexpr int kBrRegRows = 3;                // q9 = 0..2 (dj = -1) kept in registers
 constexpr int kBrSmRows = 9 - kBrRegRows;
 constexpr int kBrWinMax = 448;               // halo-window nodes
-constexpr int kBrSmemA = 3 * kBrSmRows * 9 * kBrCap;  // doubles
 constexpr int kBrFill = (3 * kBrWinMax + kBrBlock - 1) / kBrBlock;
 constexpr int kBrOwnVec = 9 * kBrLn;        // pipelined variant: [part][comp][kBrLn] SpMV partials
 constexpr int kBrStage = 2 * 160;            // pipelined variant: staged partial packets
@@ -286,6 +290,7 @@ struct BrickState {           // device-resident across launches (Pcg80::bstate)
 struct BrickArgs {
   GridDesc g;
   const double* A;     // stencil SoA (243 * nn)
+  const double* Apk;   // pipelined variants: operator packed per block (pcg80_pack_kernel)
   const double* dinv;  // node layout, 0 on fixed
   const double* b;     // node layout
   double* x;           // node layout
@@ -295,23 +300,25 @@ struct BrickArgs {
   double eps;
   int steps;
   int sx, sy, sz;
+  int nrep;            // variant 3: replicas of the partial-packet array (spread L2 polling)
+  int poll_ns;         // variant 3: back-off between polling passes
   long long* trace;
 };
 
 __device__ __forceinline__ void ll_store(uint4* a, double v, unsigned flag) {
-  asm volatile("st.volatile.global.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(a),
+  asm volatile("st.relaxed.gpu.global.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(a),
                "r"(unsigned(__double2loint(v))), "r"(flag), "r"(unsigned(__double2hiint(v))),
                "r"(flag) : "memory");
 }
 __device__ __forceinline__ uint4 ll_raw(const uint4* a) {
   uint4 v;
-  asm volatile("ld.volatile.global.v4.u32 {%0, %1, %2, %3}, [%4];"
+  asm volatile("ld.relaxed.gpu.global.v4.u32 {%0, %1, %2, %3}, [%4];"
                : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(a) : "memory");
   return v;
 }
 __device__ __forceinline__ bool ll_load(const uint4* a, unsigned flag, double& v) {
   unsigned lo, f0, hi, f1;
-  asm volatile("ld.volatile.global.v4.u32 {%0, %1, %2, %3}, [%4];"
+  asm volatile("ld.relaxed.gpu.global.v4.u32 {%0, %1, %2, %3}, [%4];"
                : "=r"(lo), "=r"(f0), "=r"(hi), "=r"(f1) : "l"(a) : "memory");
   v = __hiloint2double(int(hi), int(lo));
   return f0 == flag && f1 == flag;
@@ -430,11 +437,12 @@ __device__ __forceinline__ void br_publish2(double v0, double v1, const BrickArg
   __syncthreads();
   if (warp == 0) {
     const int nb = gridDim.x;
-    uint4* sl = P.slots + (flag & 1) * 2 * nb;
+    // every replica [parity][r][2][nb] of the packet array (P.nrep >= 1)
+    uint4* sl = P.slots + (flag & 1) * 2 * nb * P.nrep + lane * 2 * nb;
     const int nw = int((blockDim.x + 31) >> 5);
     const double s0 = wsum(lane < nw ? red[lane] : 0.0);
     const double s1 = wsum(lane < nw ? red[16 + lane] : 0.0);
-    if (lane == 0) {
+    if (lane < P.nrep) {
       ll_store(sl + blockIdx.x, s0, flag);
       ll_store(sl + nb + blockIdx.x, s1, flag);
     }
@@ -541,11 +549,69 @@ __device__ __forceinline__ void tm_ld18(uint32_t addr, double (&v)[9]) {
 //   p = z + beta p; s = w + beta s; x += alpha p; r -= alpha s; z = D^-1 r.
 // The reference's break tests map one to one: its rz_new test of step i-1 is
 // the gamma test of step i, its p.q test the p.Ap test.
+// shared-memory operator rows (doubles) and the whole dynamic allocation (bytes)
+__host__ __device__ constexpr int br_smem_a(int var) {
+  return 3 * (9 - (var >= 2 ? kBrTmRows : kBrRegRows)) * 9 * kBrCap;
+}
+__host__ __device__ constexpr int br_smem_bytes(int var) {
+  return int(sizeof(double)) * (br_smem_a(var) + 3 * kBrWinMax + kBrOwnVec) +
+         int(sizeof(uint4)) * kBrStage +
+         (var == 3 ? int(sizeof(double)) * (3 * kBrWinMax + 3 * kBrFill * kBrBlock) : 0);
+}
+
+// Operator of the pipelined variants packed per block at setup, in the order
+// the kernel consumes it: the TMEM rows as [q/2][thread][2] (one coalesced
+// 16-byte load per thread and row pair), then the shared-memory rows in the
+// exact smA layout (one bulk async copy).
+constexpr int kBrPkQ = (kBrTmRows * 9 + 1) / 2;        // double2 per thread
+constexpr int kBrPkT = 2 * kBrPkQ * kBrBlock;           // doubles
+constexpr int kBrPkS = 3 * (9 - kBrTmRows) * 9 * kBrCap;  // doubles
+constexpr int kBrPk = kBrPkT + kBrPkS;                  // doubles per block
+static_assert((kBrPkT * 8) % 16 == 0 && (kBrPkS * 8) % 16 == 0, "bulk copy alignment");
+
+__global__ void __launch_bounds__(kBrBlock) pcg80_pack_kernel(BrickArgs P, double* out) {
+  const int NX = P.g.nx + 1, NY = P.g.ny + 1, NZ = P.g.nz + 1;
+  const int nn = NX * NY * NZ;
+  const int bxi = int(blockIdx.x) % P.sx, byi = (int(blockIdx.x) / P.sx) % P.sy,
+            bzi = int(blockIdx.x) / (P.sx * P.sy);
+  const int x0 = bxi * NX / P.sx, y0 = byi * NY / P.sy, z0 = bzi * NZ / P.sz;
+  const int bx = (bxi + 1) * NX / P.sx - x0, by = (byi + 1) * NY / P.sy - y0,
+            bz = (bzi + 1) * NZ / P.sz - z0;
+  const int nloc = bx * by * bz;
+  const int t = threadIdx.x;
+  const int part = min(t / kBrCap, 2), ln = t - part * kBrCap;
+  const bool act = ln < nloc;
+  const int lnc = act ? ln : 0;
+  const int node = (x0 + lnc % bx) + NX * ((y0 + (lnc / bx) % by) + NY * (z0 + lnc / (bx * by)));
+  double* o = out + int64_t(blockIdx.x) * kBrPk;
+  for (int q = 0; q < 2 * kBrPkQ; ++q) {
+    const double v = (q < kBrTmRows * 9 && act)
+                         ? P.A[int64_t((part * 9 + q / 9) * 9 + q % 9) * nn + node] : 0.0;
+    o[((q >> 1) * kBrBlock + t) * 2 + (q & 1)] = v;
+  }
+  constexpr int kSR = 9 - kBrTmRows;
+  for (int idx = t; idx < kBrPkS; idx += blockDim.x) {
+    const int e = idx / kBrCap, l = idx % kBrCap;
+    const int pp = e / (kSR * 9), qq = (e / 9) % kSR, ent = e % 9;
+    double v = 0.0;
+    if (l < nloc) {
+      const int gn = (x0 + l % bx) + NX * ((y0 + (l / bx) % by) + NY * (z0 + l / (bx * by)));
+      v = P.A[int64_t((pp * 9 + kBrTmRows + qq) * 9 + ent) * nn + gn];
+    }
+    o[kBrPkT + idx] = v;
+  }
+}
+
+// variant 3 adds a communication warp to the kBrBlock compute threads
+__host__ __device__ constexpr int br_threads(int var) { return var == 3 ? kBrBlock + 32 : kBrBlock; }
+
 template <int kVar>
-__global__ void __launch_bounds__(kBrBlock, 1) pcg80_brick_kernel(BrickArgs P) {
+__global__ void __launch_bounds__(br_threads(kVar), 1) pcg80_brick_kernel(BrickArgs P) {
   extern __shared__ double smdyn[];
-  double* smA = smdyn;             // [(part*6 + row)*9 + entry][kBrCap]
-  double* pw = smdyn + kBrSmemA;   // [3][kBrWinMax] p on the brick + halo
+  // register (TMEM for the pipelined variants) rows / shared-memory rows
+  constexpr int kRR = kVar >= 2 ? kBrTmRows : kBrRegRows, kSR = 9 - kRR;
+  double* smA = smdyn;             // [(part*kSR + row)*9 + entry][kBrCap]
+  double* pw = smdyn + br_smem_a(kVar);  // [3][kBrWinMax] p on the brick + halo
   double* ov = pw + 3 * kBrWinMax;  // [3][3][kBrLn] SpMV partials (pipelined variant)
   uint4* pst = reinterpret_cast<uint4*>(ov + kBrOwnVec);  // [2][160] staged packets
   __shared__ double rowpart[2][3][kBrLn];
@@ -578,16 +644,26 @@ __global__ void __launch_bounds__(kBrBlock, 1) pcg80_brick_kernel(BrickArgs P) {
   const unsigned fbase = (seq + 1u) << 10;
 
   // operator rows: dj = -1 row of this thread's dk plane in registers (TMEM
-  // for the pipelined variant), the rest in shared memory
-  // register (TMEM for the pipelined variant) rows / shared-memory rows
-  constexpr int kRR = kVar == 2 ? kBrTmRows : kBrRegRows, kSR = 9 - kRR;
-  double areg[kRR * 9];
-#pragma unroll
-  for (int q = 0; q < kRR * 9; ++q)
-    areg[q] = act ? __ldg(P.A + int64_t((part * 9 + q / 9) * 9 + q % 9) * nn + node) : 0.0;
+  // for the pipelined variants), the rest in shared memory
   __shared__ uint32_t tm_base;
+  __shared__ __align__(8) unsigned long long pk_bar;
   uint32_t tm_row = 0;  // this warp's TMEM address (lane quarter, column slot)
-  if constexpr (kVar == 2) {
+  if constexpr (kVar >= 2) {
+    // packed operator: the shared-memory rows arrive by one bulk async copy
+    // (mbarrier completion) while the threads stream their TMEM rows
+    const double* blk = P.Apk + int64_t(blockIdx.x) * kBrPk;
+    const unsigned bar_s = static_cast<unsigned>(__cvta_generic_to_shared(&pk_bar));
+    if (t == 0) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar_s) : "memory");
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar_s),
+                   "n"(kBrPkS * 8) : "memory");
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+          ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(smA))), "l"(blk + kBrPkT),
+          "n"(kBrPkS * 8), "r"(bar_s) : "memory");
+    }
+    stamp_s(P.trace, 15, 0);
     const int warp = t >> 5;
     if (warp == 0) {
       asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
@@ -599,16 +675,47 @@ __global__ void __launch_bounds__(kBrBlock, 1) pcg80_brick_kernel(BrickArgs P) {
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     tm_row = tm_base + (uint32_t((warp & 3) * 32) << 16) + uint32_t((warp >> 2) * 128);
+    // TMEM rows 0..3 then 4..6: 18 / 14 coalesced 16-byte loads in flight per thread
+    const double2* src = reinterpret_cast<const double2*>(blk) + t;
+    auto rows = [&](auto q0c, auto nrc) {
+      constexpr int q0 = decltype(q0c)::value, nr = decltype(nrc)::value;
+      constexpr int np = (nr * 9 + 1) / 2;
+      double v[2 * np];
 #pragma unroll
-    for (int q = 0; q < kRR; ++q) {
-      double v[9];
+      for (int j = 0; j < np; ++j) {
+        const double2 d = __ldg(src + (q0 * 9 / 2 + j) * kBrBlock);
+        v[2 * j] = d.x;
+        v[2 * j + 1] = d.y;
+      }
 #pragma unroll
-      for (int e = 0; e < 9; ++e) v[e] = areg[q * 9 + e];
-      tm_st18(tm_row + uint32_t(q * 18), v);
+      for (int q = 0; q < nr; ++q) {
+        double r[9];
+#pragma unroll
+        for (int e = 0; e < 9; ++e) r[e] = v[q * 9 + e];
+        tm_st18(tm_row + uint32_t((q0 + q) * 18), r);
+      }
+    };
+    stamp_s(P.trace, 15, 1);
+    static_assert(kBrTmRows == 7, "row chunks below");
+    if (warp < kBrBlock / 32) {  // (not the communication warp of variant 3)
+      rows(std::integral_constant<int, 0>{}, std::integral_constant<int, 4>{});
+      rows(std::integral_constant<int, 4>{}, std::integral_constant<int, 3>{});
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
     }
-    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+    stamp_s(P.trace, 15, 2);
+    // shared-memory rows landed (phase 0 of the bulk-copy barrier)
+    asm volatile(
+        "{\n .reg .pred p;\n WAIT_%=:\n"
+        " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n"
+        " @!p bra WAIT_%=;\n}" ::"r"(bar_s) : "memory");
   }
-  for (int idx = t; idx < 3 * kSR * 9 * kBrCap; idx += blockDim.x) {
+  double areg[kRR * 9];  // variants 0/1 only
+  if constexpr (kVar < 2) {
+#pragma unroll
+    for (int q = 0; q < kRR * 9; ++q)
+      areg[q] = act ? __ldg(P.A + int64_t((part * 9 + q / 9) * 9 + q % 9) * nn + node) : 0.0;
+  }
+  for (int idx = t; kVar < 2 && idx < 3 * kSR * 9 * kBrCap; idx += blockDim.x) {
     const int e = idx / kBrCap, l = idx % kBrCap;
     const int pp = e / (kSR * 9), qq = (e / 9) % kSR, ent = e % 9;
     double v = 0.0;
@@ -700,7 +807,7 @@ __global__ void __launch_bounds__(kBrBlock, 1) pcg80_brick_kernel(BrickArgs P) {
   };
   auto spmv = [&](double av[3]) { spmv_mid(av, [] {}); };
 
-  if constexpr (kVar == 2) {
+  if constexpr (kVar >= 2) {
     // Component ownership: thread (part, ln) owns component c = part of node
     // ln, so the ten per-DOF recurrences are scalars in every thread (no
     // 3-wide owner arrays: the registers go to the SpMV's load pipeline).
@@ -713,11 +820,17 @@ __global__ void __launch_bounds__(kBrBlock, 1) pcg80_brick_kernel(BrickArgs P) {
     // added in part order (p0 + p1) + p2 by every consumer
     // (two accumulators per row -- register rows / shared rows -- halve the
     // dependent DFMA chains)
-    auto spmv_own = [&](auto&& mid) {
+    // compute-warp barrier (variant 3 has a communication warp outside it)
+    auto csync = [&] {
+      if constexpr (kVar == 3) asm volatile("bar.sync 3, %0;" ::"n"(kBrBlock) : "memory");
+      else __syncthreads();
+    };
+    // mid() is called before stencil row qmid (the partial-packet staging hook)
+    auto spmv_own_at = [&](auto qmid, auto&& mid) {
       double acc[2][3] = {{0.0, 0.0, 0.0}, {0.0, 0.0, 0.0}};
 #pragma unroll
       for (int q9 = 0; q9 < 9; ++q9) {
-        if (q9 == kMidQ) mid();
+        if (q9 == decltype(qmid)::value) mid();
         const int w = wbase + (q9 / 3) * WX + q9 % 3;
         const double pv0 = pw[w], pv1 = pw[kBrWinMax + w], pv2 = pw[2 * kBrWinMax + w];
         double a[9];
@@ -742,9 +855,356 @@ __global__ void __launch_bounds__(kBrBlock, 1) pcg80_brick_kernel(BrickArgs P) {
       rp3[(part * 3 + 0) * kBrLn + ln] = acc[0][0] + acc[1][0];
       rp3[(part * 3 + 1) * kBrLn + ln] = acc[0][1] + acc[1][1];
       rp3[(part * 3 + 2) * kBrLn + ln] = acc[0][2] + acc[1][2];
-      __syncthreads();
+      csync();
       return (rp3[c * kBrLn + ln] + rp3[(3 + c) * kBrLn + ln]) + rp3[(6 + c) * kBrLn + ln];
     };
+    auto spmv_own = [&](auto&& mid) {
+      return spmv_own_at(std::integral_constant<int, kMidQ>{}, mid);
+    };
+    auto tm_free = [&] {
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncthreads();
+      if (t < 32)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tm_base),
+                     "n"(kBrTmemCols) : "memory");
+    };
+    // collect the (gamma, delta) partial packets of flag pf staged in pst
+    // (re-polling stale ones), summed in a fixed order: identical on every block
+    auto collect_staged = [&](unsigned pf, double& gam, double& del) {
+      const uint4* sl = P.slots + (pf & 1) * 2 * nb;
+      if (t < 32) {
+        asm volatile("cp.async.wait_all;" ::: "memory");
+        __syncwarp();
+        double a0[5], a1[5];
+        bool ok[10];
+#pragma unroll
+        for (int k = 0; k < 5; ++k) {
+          const int bb = t + 32 * k;
+          a0[k] = 0.0;
+          a1[k] = 0.0;
+          ok[2 * k] = ok[2 * k + 1] = true;
+          if (bb < nb) {
+            const uint4 v0 = pst[bb], v1 = pst[nb + bb];
+            ok[2 * k] = v0.y == pf && v0.w == pf;
+            ok[2 * k + 1] = v1.y == pf && v1.w == pf;
+            a0[k] = __hiloint2double(int(v0.z), int(v0.x));
+            a1[k] = __hiloint2double(int(v1.z), int(v1.x));
+          }
+        }
+        bool all = true;
+#pragma unroll
+        for (int k = 0; k < 10; ++k) all = all && ok[k];
+        while (!all) {
+          uint4 v[10];
+#pragma unroll
+          for (int k = 0; k < 10; ++k)
+            if (!ok[k]) v[k] = ll_raw(sl + (k & 1) * nb + t + 32 * (k >> 1));
+          all = true;
+#pragma unroll
+          for (int k = 0; k < 10; ++k) {
+            if (!ok[k]) {
+              ok[k] = v[k].y == pf && v[k].w == pf;
+              if (ok[k]) {
+                const double d = __hiloint2double(int(v[k].z), int(v[k].x));
+                if (k & 1) a1[k >> 1] = d; else a0[k >> 1] = d;
+              }
+            }
+            all = all && ok[k];
+          }
+        }
+        const double r0 = wsum(a0[0] + a0[1] + a0[2] + a0[3] + a0[4]);
+        const double r1 = wsum(a1[0] + a1[1] + a1[2] + a1[3] + a1[4]);
+        if (t == 0) {
+          tot2[0] = r0;
+          tot2[1] = r1;
+        }
+      }
+      __syncthreads();
+      gam = tot2[0];
+      del = tot2[1];
+    };
+    auto stage_partials = [&](unsigned pf) {
+      if (t < 32) {
+        const uint4* sl = P.slots + (pf & 1) * 2 * nb;
+        for (int q = t; q < 2 * nb; q += 32) {
+          const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(pst + q));
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(sl + q) : "memory");
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+      }
+    };
+    if constexpr (kVar == 3) {
+      stamp_s(P.trace, 15, 3);
+      // Early-halo pipelined CG with a communication warp.
+      //  * Same recurrences as kVar = 2, but what crosses blocks is the raw
+      //    SpMV result nv = A m of the brick, sent the moment the SpMV is done.
+      //    Every block keeps the z and w recurrences for its whole halo window
+      //    (fill cells) and forms the next m there itself,
+      //    m' = D^-1 (w - alpha (fma(eps, m, nv) + beta z)), with the same
+      //    expressions on the same bits as the owner, so the L2 round trip of
+      //    the halo overlaps the all-reduce collect and the scalar update.
+      //  * Warp kBrBlock/32 (the communication warp) owns the all-reduce: it
+      //    forms and publishes the block partials, then polls every block's
+      //    packets while the 14 compute warps run the next SpMV; the compute
+      //    warps only wait on named barrier 2 for the result.
+      //      barrier 1: compute warps arrive (per-warp partials in red[]),
+      //                 comm warp syncs;
+      //      barrier 2: comm warp arrives ((gamma, delta) in tot2), compute
+      //                 warps sync;
+      //      barrier 3: compute warps only (the SpMV partials, end of step).
+      //  * Window m double-buffered; beta and gamma/alpha_prev use reciprocals
+      //    formed after the fill (one division on the collect -> fill path).
+      constexpr int kCompute = kBrBlock;
+      const bool comm = t >= kCompute;
+      double* pwA = pw;
+      double* pwB = reinterpret_cast<double*>(pst + kBrStage);
+      // fill cells: window index fw, LL index fg (halo) or rp3 index fo (own)
+      // per fill cell recurrences in shared memory ([k][thread], conflict-free)
+      int fo[kBrFill];
+      double* fzh = pwB + 3 * kBrWinMax;
+      double* fwh = fzh + kBrFill * kBrBlock;
+      double* fdv = fwh + kBrFill * kBrBlock;
+#define ZH(k) fzh[(k) * kBrBlock + t]
+#define WH(k) fwh[(k) * kBrBlock + t]
+#define DVH(k) fdv[(k) * kBrBlock + t]
+      __shared__ int stop;
+      if (t == 0) stop = 0;
+#pragma unroll
+      for (int k = 0; k < kBrFill; ++k) {
+        fo[k] = -1;
+        if (comm) continue;
+        ZH(k) = 0.0;
+        WH(k) = 0.0;
+        DVH(k) = 0.0;
+        const int iw = t + k * kBrBlock;
+        if (iw < 3 * wn) {
+          const int cc = iw / wn, w = iw - cc * wn;
+          const int wx = w % WX, wy = (w / WX) % WY, wz = w / (WX * WY);
+          if (wx >= 1 && wx <= bx && wy >= 1 && wy <= by && wz >= 1 && wz <= bz) {
+            fo[k] = cc * kBrLn + (wx - 1) + bx * ((wy - 1) + by * (wz - 1));
+          }
+          double u0 = 0.0;
+          if (fg[k] >= 0) {
+            const int gnode = fg[k] - cc * nn;
+            const double d = P.dinv[3 * gnode + cc];
+            DVH(k) = d;
+            u0 = d * P.b[3 * gnode + cc];
+          }
+          pwA[fw[k]] = u0;
+          pwB[fw[k]] = 0.0;
+          WH(k) = u0;  // holds u0 until the first fill turns it into w0
+        }
+      }
+      if (act) {
+        rr = P.b[3 * node + c];
+        dv = P.dinv[3 * node + c];
+        uu = dv * rr;
+      }
+      __syncthreads();
+      stamp_s(P.trace, 15, 4);
+
+      if (comm) {
+        // ---------------------------------------------- communication warp
+        const int lane = t - kCompute;
+        constexpr int nw = kCompute / 32;
+        unsigned epoch = 0;
+        for (int s = 0; s < P.steps; ++s) {
+          asm volatile("bar.sync 1, %0;" ::"n"(kCompute + 32) : "memory");
+          if (stop) break;
+          ++epoch;
+          const unsigned pf = fbase | epoch;
+          // replica r of the packet array: [parity][r][2][nb]; every block
+          // writes all replicas, polls replica blockIdx % nrep
+          uint4* sl0 = P.slots + (pf & 1) * 2 * nb * P.nrep;
+          uint4* sl = sl0 + (int(blockIdx.x) % P.nrep) * 2 * nb;
+          const double s0 = wsum(lane < nw ? red[lane] : 0.0);
+          const double s1 = wsum(lane < nw ? red[16 + lane] : 0.0);
+          if (lane < P.nrep) {
+            ll_store(sl0 + lane * 2 * nb + blockIdx.x, s0, pf);
+            ll_store(sl0 + lane * 2 * nb + nb + blockIdx.x, s1, pf);
+          }
+          // poll every block's packets (all loads of a pass in flight)
+          double a0[5], a1[5];
+          bool ok[10];
+#pragma unroll
+          for (int k = 0; k < 10; ++k) ok[k] = lane + 32 * (k >> 1) >= nb;
+#pragma unroll
+          for (int k = 0; k < 5; ++k) a0[k] = a1[k] = 0.0;
+          bool all;
+          do {
+            uint4 v[10];
+#pragma unroll
+            for (int k = 0; k < 10; ++k)
+              if (!ok[k]) v[k] = ll_raw(sl + (k & 1) * nb + lane + 32 * (k >> 1));
+            all = true;
+#pragma unroll
+            for (int k = 0; k < 10; ++k) {
+              if (!ok[k]) {
+                ok[k] = v[k].y == pf && v[k].w == pf;
+                if (ok[k]) {
+                  const double d = __hiloint2double(int(v[k].z), int(v[k].x));
+                  if (k & 1) a1[k >> 1] = d; else a0[k >> 1] = d;
+                }
+              }
+              all = all && ok[k];
+            }
+            if (P.poll_ns && !all) __nanosleep(P.poll_ns);
+          } while (!__all_sync(0xffffffffu, all));
+          const double r0 = wsum(a0[0] + a0[1] + a0[2] + a0[3] + a0[4]);
+          const double r1 = wsum(a1[0] + a1[1] + a1[2] + a1[3] + a1[4]);
+          if (lane == 0) {
+            tot2[0] = r0;
+            tot2[1] = r1;
+          }
+          __syncwarp();
+          asm volatile("bar.arrive 2, %0;" ::"n"(kCompute + 32) : "memory");
+        }
+      } else {
+        // --------------------------------------------------- compute warps
+        // w0 = A u0 + eps u0: no exchange needed (u0 is local data everywhere)
+        double nv = spmv_own([] {});
+        stamp_s(P.trace, 15, 5);
+        if (act) {
+          ww = fma(P.eps, uu, nv);
+          ll_store(P.zll + c * nn + node, nv, fbase);
+        }
+        // per-warp partials of (gamma, delta) = (r.u, w.u) -> comm warp
+        auto to_comm = [&](double lg, double ld) {
+          lg = wsum(lg);
+          ld = wsum(ld);
+          if ((t & 31) == 0) {
+            red[t >> 5] = lg;
+            red[16 + (t >> 5)] = ld;
+          }
+          asm volatile("bar.arrive 1, %0;" ::"n"(kCompute + 32) : "memory");
+        };
+        to_comm(act ? rr * uu : 0.0, act ? ww * uu : 0.0);
+        // halo cells: the LL loads are issued early (halo_issue, right after
+        // the collect) and validated late (halo_finish), so their L2 round trip
+        // overlaps the scalar update; own cells read the block's SpMV partials
+        // from shared memory.  halo_issue only issues the loads: the flag test
+        // -- the first use of the loaded registers -- is in halo_finish.
+        uint4 zraw[kBrFill];
+        auto halo_issue = [&](unsigned ph) {
+          const uint4* base = P.zll + (ph & 1) * nn3;
+#pragma unroll
+          for (int k = 0; k < kBrFill; ++k) {
+            zraw[k] = make_uint4(0u, 0u, 0u, 0u);
+            if (fo[k] < 0 && fg[k] >= 0) zraw[k] = ll_raw(base + fg[k]);
+          }
+        };
+        auto halo_finish = [&](unsigned ph, double* dst, auto&& upd) {
+          const uint4* base = P.zll + (ph & 1) * nn3;
+          const unsigned zf = fbase + ph;
+          double zv[kBrFill];
+          bool zok[kBrFill];
+          bool all = true;
+#pragma unroll
+          for (int k = 0; k < kBrFill; ++k) {
+            zok[k] = !(fo[k] < 0 && fg[k] >= 0) || (zraw[k].y == zf && zraw[k].w == zf);
+            zv[k] = __hiloint2double(int(zraw[k].z), int(zraw[k].x));
+            all = all && zok[k];
+          }
+          while (!all) {
+            all = true;
+#pragma unroll
+            for (int k = 0; k < kBrFill; ++k) {
+              if (!zok[k]) zok[k] = ll_load(base + fg[k], zf, zv[k]);
+              all = all && zok[k];
+            }
+          }
+#pragma unroll
+          for (int k = 0; k < kBrFill; ++k) {
+            if (fo[k] >= 0) {
+              const int o = fo[k] % kBrLn, cc = fo[k] / kBrLn;
+              zv[k] = (rp3[cc * kBrLn + o] + rp3[(3 + cc) * kBrLn + o]) + rp3[(6 + cc) * kBrLn + o];
+            }
+            if (fg[k] >= 0) dst[fw[k]] = upd(k, zv[k]);
+          }
+        };
+        // window: w0 = fma(eps, u0, nv0), m0 = D^-1 w0
+        halo_issue(0u);
+        halo_finish(0u, pwB, [&](int k, double v) {
+          const double w = fma(P.eps, WH(k), v);
+          WH(k) = w;
+          return DVH(k) * w;
+        });
+        csync();
+        stamp_s(P.trace, 15, 6);
+        double igprev = 0.0, iaprev = 0.0;
+        for (int s = 0; s < P.steps; ++s) {
+          double* cur = (s & 1) ? pwA : pwB;  // m_s
+          double* nxt = (s & 1) ? pwB : pwA;  // m_{s+1}
+          pw = cur;
+          const int ts = s == 15 ? -1 : s;  // trace slot 15 holds the prologue stamps
+          stamp_s(P.trace, ts, 0);
+          nv = spmv_own([] {});
+          if (act) ll_store(P.zll + ((s + 1) & 1) * nn3 + c * nn + node, nv, fbase + unsigned(s) + 1u);
+          stamp_s(P.trace, ts, 3);
+          asm volatile("bar.sync 2, %0;" ::"n"(kCompute + 32) : "memory");
+          const double gam = tot2[0], del = tot2[1];
+          stamp_s(P.trace, ts, 2);
+          if (s + 1 < P.steps) halo_issue(unsigned(s) + 1u);
+          double beta = 0.0, pap = del;
+          bool brk = false;
+          if (s > 0) {
+            brk = !(gam > 0.0) || !isfinite(gam);
+            beta = gam * igprev;
+            pap = del - (beta * gam) * iaprev;
+          }
+          brk = brk || !(pap > 0.0) || !isfinite(pap);
+          if (brk) {  // identical on every block; release the comm warp
+            if (t == 0) stop = 1;
+            csync();
+            asm volatile("bar.arrive 1, %0;" ::"n"(kCompute + 32) : "memory");
+            break;
+          }
+          const double al = gam / pap;
+          stamp_s(P.trace, ts, 7);
+          double lg = 0.0, ld = 0.0;
+          if (act) {
+            const double mv = cur[c * kBrWinMax + wctr];
+            const double n = fma(P.eps, mv, nv);
+            zz = fma(beta, zz, n);
+            qq = fma(beta, qq, mv);
+            ss = fma(beta, ss, ww);
+            pp = fma(beta, pp, uu);
+            xr = fma(al, pp, xr);
+            rr = fma(-al, ss, rr);
+            uu = fma(-al, qq, uu);
+            ww = fma(-al, zz, ww);
+            lg = rr * uu;
+            ld = ww * uu;
+          }
+          if (s + 1 == P.steps) break;
+          to_comm(lg, ld);
+          stamp_s(P.trace, ts, 1);
+          halo_finish(unsigned(s) + 1u, nxt, [&](int k, double v) {
+            const double n = fma(P.eps, cur[fw[k]], v);
+            const double z = fma(beta, ZH(k), n);
+            const double w = fma(-al, z, WH(k));
+            ZH(k) = z;
+            WH(k) = w;
+            return DVH(k) * w;
+          });
+          stamp_s(P.trace, ts, 5);
+          igprev = 1.0 / gam;
+          iaprev = 1.0 / al;
+          csync();
+          stamp_s(P.trace, ts, 4);
+        }
+        if (act) P.x[3 * node + c] = xr;
+        if (blockIdx.x == 0 && t == 0) {
+          P.st->origin = c0;
+          P.st->seq = seq + 1u;
+        }
+      }
+      tm_free();
+      return;
+#undef ZH
+#undef WH
+#undef DVH
+    }
     // phase 0: u0 = D^-1 b (flag fbase, buffer 0); w0 = A u0
     if (act) {
       rr = P.b[3 * node + c];
@@ -803,7 +1263,7 @@ __global__ void __launch_bounds__(kBrBlock, 1) pcg80_brick_kernel(BrickArgs P) {
       // stage every block's partial packets into shared memory while the SpMV
       // runs (cp.async, L2 path); validated and re-polled afterwards
       const unsigned pf = fbase | epoch;
-      const uint4* sl = P.slots + (pf & 1) * 2 * nb;
+      const uint4* sl = P.slots + (pf & 1) * 2 * nb * P.nrep + (int(blockIdx.x) % P.nrep) * 2 * nb;
       // (issued two thirds into the SpMV, so late publishers are caught)
       const double nv = spmv_own([&] {
         if (t < 32) {
@@ -1105,20 +1565,41 @@ void Pcg80::setup(const Grid& g, const double* A, const double* diag, double eps
   if (planned) {
     brick = true;
     nblocks = sx * sy * sz;
-    smem_bytes = int(sizeof(double)) * (kBrSmemA + 3 * kBrWinMax + kBrOwnVec) +
-                 int(sizeof(uint4)) * kBrStage;
-    SG_REQUIRE(smem_bytes <= smem_optin, "pcg80 brick kernel shared memory");
     // 0: Hestenes-Stiefel (two all-reduces per step), 1: Chronopoulos-Gear,
-    // 2: pipelined (the all-reduce hidden behind the SpMV)
-    variant = getenv("SG_PCG80_HS") ? 0 : getenv("SG_PCG80_CG") ? 1 : 2;
-    void* fns[3] = {(void*)pcg80_brick_kernel<0>, (void*)pcg80_brick_kernel<1>,
-                    (void*)pcg80_brick_kernel<2>};
-    for (void* fn : fns)
-      SG_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes));
-    SG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fns[variant], kBrBlock,
+    // 2: pipelined (the all-reduce hidden behind the SpMV; default), 3:
+    // pipelined with the halo sent straight after the SpMV and a
+    // communication warp for the all-reduce (measured slower: DESIGN 6b)
+    variant = getenv("SG_PCG80_HS") ? 0 : getenv("SG_PCG80_CG") ? 1
+            : getenv("SG_PCG80_EARLY") ? 3 : 2;
+    constexpr int kBytes[4] = {br_smem_bytes(0), br_smem_bytes(1), br_smem_bytes(2),
+                               br_smem_bytes(3)};
+    smem_bytes = kBytes[variant];
+    SG_REQUIRE(smem_bytes <= smem_optin, "pcg80 brick kernel shared memory");
+    void* fns[4] = {(void*)pcg80_brick_kernel<0>, (void*)pcg80_brick_kernel<1>,
+                    (void*)pcg80_brick_kernel<2>, (void*)pcg80_brick_kernel<3>};
+    SG_CUDA(cudaFuncSetAttribute(fns[variant], cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 smem_bytes));
+    SG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fns[variant], br_threads(variant),
                                                           smem_bytes));
     SG_REQUIRE(per_sm >= 1, "pcg80 brick kernel cannot be resident");
-    slots.alloc(size_t(4 * nblocks));
+    if (variant >= 2) {
+      apk.alloc(size_t(nblocks) * kBrPk);
+      BrickArgs a{};
+      a.g = g.d;
+      a.A = A;
+      a.sx = sx;
+      a.sy = sy;
+      a.sz = sz;
+      pcg80_pack_kernel<<<nblocks, kBrBlock, 0, s>>>(a, apk.p);
+      SG_CHECK_LAUNCH();
+    }
+    nrep = 1;
+    poll_ns = 0;
+    if (variant >= 2) {
+      if (getenv("SG_PCG80_NREP")) nrep = std::max(1, std::min(32, atoi(getenv("SG_PCG80_NREP"))));
+      if (getenv("SG_PCG80_POLLNS")) poll_ns = std::max(0, atoi(getenv("SG_PCG80_POLLNS")));
+    }
+    slots.alloc(size_t(4 * nblocks * nrep));
     slots.zero(s);
     zll.alloc(size_t(6 * g.d.nnodes()));  // two LL parity buffers (pipelined variant)
     zll.zero(s);
@@ -1151,6 +1632,7 @@ void Pcg80::solve(const double* b, double* x, cudaStream_t s) {
     BrickArgs a;
     a.g = grid->d;
     a.A = Aptr;
+    a.Apk = apk.p;
     a.dinv = dinv.p;
     a.b = b;
     a.x = x;
@@ -1162,11 +1644,14 @@ void Pcg80::solve(const double* b, double* x, cudaStream_t s) {
     a.sx = sx;
     a.sy = sy;
     a.sz = sz;
+    a.nrep = nrep;
+    a.poll_ns = poll_ns;
     a.trace = trace;
     void* args[] = {&a};
-    void* fn = variant == 2 ? (void*)pcg80_brick_kernel<2>
+    void* fn = variant == 3 ? (void*)pcg80_brick_kernel<3>
+             : variant == 2 ? (void*)pcg80_brick_kernel<2>
              : variant == 1 ? (void*)pcg80_brick_kernel<1> : (void*)pcg80_brick_kernel<0>;
-    SG_CUDA(cudaLaunchCooperativeKernel(fn, dim3(nblocks), dim3(kBrBlock),
+    SG_CUDA(cudaLaunchCooperativeKernel(fn, dim3(nblocks), dim3(br_threads(variant)),
                                         args, size_t(smem_bytes), s));
     SG_CHECK_LAUNCH();
     return;

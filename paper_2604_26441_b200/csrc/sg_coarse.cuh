@@ -19,7 +19,9 @@ struct Pcg80 {
   bool brick = false;
   int variant = 2;  // 0 Hestenes-Stiefel, 1 Chronopoulos-Gear, 2 pipelined (sg_coarse.cu)
   int sx = 0, sy = 0, sz = 0;
+  int nrep = 1, poll_ns = 0;  // variant 3 all-reduce tuning (sg_coarse.cu)
   DBuf<uint4> slots, zll;
+  DBuf<double> apk;  // operator packed per brick (pipelined variants)
   DBuf<unsigned long long> bstate;
   void setup(const Grid& g, const double* A, const double* diag, double eps, int steps,
              cudaStream_t s);

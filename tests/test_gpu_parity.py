@@ -232,9 +232,16 @@ def test_config1_40cube_fp32_gmg_golden():
     np.testing.assert_allclose(op.compliance(rep.x), float(z["compliance"][0]), rtol=1e-6)
 
 
+PCG80_VARIANTS = [None, "SG_PCG80_EARLY", "SG_PCG80_HS", "SG_PCG80_CG"]
+
+
+@pytest.mark.parametrize("variant", PCG80_VARIANTS)
 @pytest.mark.parametrize("dims,kind", [((24, 16, 12), "binary"), ((20, 20, 20), "uniform")])
-def test_pcg80_brick_vs_oracle(dims, kind):
-    """Coarsest pcg80 on a many-brick split (hierarchy.py:139-162) against the oracle."""
+def test_pcg80_brick_vs_oracle(dims, kind, variant, monkeypatch):
+    """Coarsest pcg80 on a many-brick split (hierarchy.py:139-162) against the oracle,
+    every brick-kernel recurrence (default: pipelined)."""
+    if variant:
+        monkeypatch.setenv(variant, "1")
     g, op, og, E, ke = _pair(dims, kind)
     h = P.build_hierarchy(op, 3, "fp64", cholesky_cutoff=0)
     oh = O.Hier(og, E, ke, 3, "fp64", cutoff=0)
@@ -243,9 +250,12 @@ def test_pcg80_brick_vs_oracle(dims, kind):
     assert _rel(h.vcycle(r), oh.vcycle(r)) < 1e-9
 
 
-def test_pcg80_brick_matches_range_kernel_100cube(monkeypatch):
+@pytest.mark.parametrize("variant", PCG80_VARIANTS)
+def test_pcg80_brick_matches_range_kernel_100cube(variant, monkeypatch):
     """configs[3] coarsest level (26^3 nodes, 50,700 DOFs): the brick-partitioned
     kernel and the contiguous-range kernel solve the same fixed 80-step PCG."""
+    if variant:
+        monkeypatch.setenv(variant, "1")
     N = 100
     g = P.build_cantilever(N, N, N)
     op = P.FineOperator(g, P.simp_modulus(P.make_state("uniform", N, N, N, vf=0.5), 3.0))
@@ -254,6 +264,8 @@ def test_pcg80_brick_matches_range_kernel_100cube(monkeypatch):
         hb = P.build_hierarchy(op, 4, "fp32")
         monkeypatch.setenv("SG_PCG80_RANGE", "1")
         hr = P.build_hierarchy(op, 4, "fp32")
+        if variant:
+            monkeypatch.delenv(variant)
     r = P.SplitMix64(5).gaussian(g.n_free)
     zb, zr = hb.vcycle(r), hr.vcycle(r)
     # the brick kernel runs the pipelined (Ghysels-Vanroose) recurrence of the

@@ -2,7 +2,7 @@
 pipelined brick kernel (%globaltimer stamps; sg_hier_pcg80_trace).
 stamps: 0 step start, 1 published (m + partials), 5 halo filled, 3 SpMV done,
 6 partial packets validated (warp 0), 2 (gamma, delta) known, 4 update done."""
-import sys, warnings
+import os, sys, warnings
 sys.path.insert(0, ".")
 import numpy as np
 import paper_2604_26441_b200 as P
@@ -21,7 +21,7 @@ for rep in range(2):
     _native.check(lib.sg_hier_pcg80_trace(h._hh, t.ctypes.data, _dev.stream()))
     t = t.reshape(256, 8, 8)
     nb = int((t[:, 0, 0] > 0).sum())
-    t = t[:nb].astype(np.float64) / 1e3  # us
+    t = t[:nb].astype(np.float64) / (1.965e3 if os.environ.get("SG_TRACE_CLOCK") else 1e3)  # us
     starts = t[:, :, 0]
     period = np.diff(starts, axis=1)  # block x 7
     print(f"rep {rep}: blocks {nb}; step period med {np.median(period):.3f} us "
@@ -33,3 +33,11 @@ for rep in range(2):
         print(f"  {name:9s} med {np.median(d):6.3f}  p90 {np.percentile(d, 90):6.3f}  max {d.max():6.3f} us")
         prev = k
     # global step boundary: first block start to last block start of next step
+    # offsets of every stamp from the block's step start, in time order
+    # (the early-halo variant stamps 0 start, 3 SpMV, 2 collect, 1 publish, 5 fill, 4 end)
+    rel = {k: np.median(t[:, :, k] - t[:, :, 0]) for k in range(8) if (t[:, :, k] > 0).all()}
+    print("  offsets: " + ", ".join(f"{k}:{v:.2f}" for k, v in sorted(rel.items(), key=lambda kv: kv[1])))
+    # prologue (early-halo variant, slot 15): 0 entry, 1 TMEM allocated, 2 TMEM rows
+    # stored, 3 bulk copy landed + fill cells, 4 before the first SpMV, 5 after it, 6 window m0
+    p = t[:, 7, :7] - t[:, 7, :1]
+    print("  prologue: " + ", ".join(f"{k}:{np.median(p[:, k]):.2f}" for k in range(7)))
