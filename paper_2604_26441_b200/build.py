@@ -28,6 +28,8 @@ FLAGS = ["-std=c++17", "-O3", "-lineinfo", "--expt-relaxed-constexpr",
          "-Xcompiler", "-fPIC,-ffp-contract=off", "-I", INCLUDE]
 # development aid only (e.g. -DSG_TRACE_CLOCK for cycle-resolution pcg80 traces)
 FLAGS += os.environ.get("SG_NVCC_EXTRA", "").split()
+# per-file extra flags (none at present)
+FILE_FLAGS: dict = {}
 
 
 def _sources():
@@ -41,12 +43,13 @@ def _fingerprint():
             h.update(os.path.basename(path).encode())
             h.update(fh.read())
     h.update(" ".join(ARCH + FLAGS).encode())
+    h.update(repr(sorted(FILE_FLAGS.items())).encode())
     return h.hexdigest()
 
 
 def _compile(src):
     obj = os.path.join(OUT_DIR, os.path.basename(src)[:-3] + ".o")
-    cmd = [NVCC, *ARCH, *FLAGS, "-c", src, "-o", obj]
+    cmd = [NVCC, *ARCH, *FLAGS, *FILE_FLAGS.get(os.path.basename(src), []), "-c", src, "-o", obj]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"nvcc failed for {src}:\n{r.stdout}\n{r.stderr}")

@@ -703,8 +703,12 @@ extern "C" int sg_hier_profile(sg_hier* h, int what, int reps, double* ms_avg, v
     sg::DBuf<float> pa(n32), pb(n32);
     pa.zero(s);
     sg::DBuf<uint8_t> flush(size_t(256) << 20);
-    SG_CUDA(cudaMemsetAsync(a.p, 0, sizeof(double) * nd0, s));
-    SG_CUDA(cudaMemsetAsync(fa.p, 0, sizeof(float) * nd0, s));
+    // inputs: seeded unit gaussian vectors (free DOFs; fixed entries 0), not zeros
+    sg::fill_gaussian_unit(*L0.g, 12345u, a.p, H.red, H.scal.p + 3, s);
+    sg::cvt_f64_to_f32(nd0, a.p, fa.p, s);
+    if (sg::p32_supported(*H.fine)) sg::to_p32<double>(H.fine->grid.d, a.p, pa.p, s);
+    for (size_t l = 1; l < H.lv.size(); ++l)
+      sg::fill_gaussian_unit(*H.lv[l]->g, 777u + l, H.lv[l]->w.r.p, H.red, H.scal.p + 3, s);
     cudaEvent_t e0, e1;
     SG_CUDA(cudaEventCreate(&e0));
     SG_CUDA(cudaEventCreate(&e1));
@@ -740,6 +744,13 @@ extern "C" int sg_hier_profile(sg_hier* h, int what, int reps, double* ms_avg, v
           sg::Level& L = *H.lv[0];
           sg::fine_apply_p32_cheb(*H.fine, L.w.x32.p, L.w.x32b.p, L.w.b32.p, L.dinv32p.p, L.w.dd32.p,
                                   0.5f, 0.25f, false, s);
+          break;
+        }
+        case 7: {  // the fused level-0 apply + residual the V-cycle runs (P32 -> node f64)
+          SG_REQUIRE(H.lv[0]->p32, "level 0 is not in the P32 layout");
+          sg::Level& L = *H.lv[0];
+          sg::fine_apply_p32_res(*H.fine, pa.p, a.p, b.p, s);
+          (void)L;
           break;
         }
         default: throw sg::Error("unknown profile target");

@@ -12,9 +12,9 @@ for tool in memcheck racecheck synccheck initcheck; do
       > gpurun_out/sanitize_$tool.txt 2>&1
   echo "$tool rc=$?" >> gpurun_out/sanitize_rc.txt
 done
-# synccheck reports "Barrier error ... Missing init" at shared address 0 in the
-# TMEM-resident pipelined pcg80 kernel (no mbarrier in that kernel: the
-# tcgen05.alloc result slot); re-run the same test on the variants without TMEM
+# (round 1 saw a synccheck "Missing init" report at shared address 0 of the
+# pipelined pcg80 kernel; round 2: 0 errors for every variant) -- the
+# variants without TMEM are re-run as well
 for v in SG_PCG80_HS SG_PCG80_CG; do
   env $v=1 timeout 900 $CS --tool synccheck --print-limit 5 --error-exitcode 0 \
       python -m pytest tests/test_gpu_parity.py -m gpu -q -x -k "pcg80_and_dense or pcg80_brick_vs" \
