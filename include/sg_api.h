@@ -250,6 +250,16 @@ int sg_vec_div(int dtype, int64_t n, const void* a, double s, void* c, void* str
 int sg_vec_bf16(int64_t n, const float* a, float* b, void* stream);
 
 /* ---------------------------------------------------------------------
+ * Fixtures on the device
+ * make_state (states.py:58-111) drawn into HBM from the splitmix64 stream
+ * (prng.py:20-52): rho = device, nx*ny*nz doubles; kind = index into
+ * STATE_KINDS (0 uniform, 1 binary, 2 checkerboard, 3 layered,
+ * 4 random_floor, 5 mixed_near_void).  Bit-identical to the host generator.
+ * ------------------------------------------------------------------- */
+int sg_make_state(int kind, int nx, int ny, int nz, double vf, double floor_, uint64_t seed,
+                  double* rho, void* stream);
+
+/* ---------------------------------------------------------------------
  * Host-only work plans (no device needed; used by the CPU tests).
  * sg_plan_brick: pcg80 brick split of the coarsest node grid -> {sx, sy, sz}
  *   ({0,0,0}: no split fits, the contiguous-range kernel runs).

@@ -118,6 +118,8 @@ SIGNATURES = {
     "sg_vec_scale": (c_int, [c_int, c_i64, c_void_p, c_double, c_void_p, c_void_p]),
     "sg_vec_div": (c_int, [c_int, c_i64, c_void_p, c_double, c_void_p, c_void_p]),
     "sg_vec_bf16": (c_int, [c_i64, c_void_p, c_void_p, c_void_p]),
+    "sg_make_state": (c_int, [c_int, c_int, c_int, c_int, c_double, c_double, c_u64, c_void_p,
+                              c_void_p]),
 }
 
 _lib = None

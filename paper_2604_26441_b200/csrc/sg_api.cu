@@ -602,6 +602,16 @@ int sg_vec_bf16(int64_t n, const float* a, float* b, void* stream) {
   });
 }
 
+int sg_make_state(int kind, int nx, int ny, int nz, double vf, double floor_, uint64_t seed,
+                  double* rho, void* stream) {
+  return guard([&] {
+    SG_REQUIRE(kind >= 0 && kind <= 5, "unknown state kind");
+    SG_REQUIRE(nx > 0 && ny > 0 && nz > 0 && rho, "bad fixture arguments");
+    sg::make_state_device(kind, nx, ny, nz, vf, floor_, static_cast<unsigned long long>(seed), rho,
+                          S(stream));
+  });
+}
+
 }  // extern "C"
 
 // ------------------------------------------------- standalone transfers
