@@ -108,8 +108,12 @@ void fine_apply_dense_f64(const FineOp& op, const double* u, double* y, cudaStre
 void fine_apply_dense_f32(const FineOp& op, const float* u, float* y, cudaStream_t s) {
   launch_apply<float, 1>(op.grid.d, op.grid.nmask.p, u, y, op.E32.p, op.ke32, s);
 }
+// FP64: the block-form Walsh kernel with plane-shared transforms
+// (sg_fine_p64.cu); SG_WALSH64_OLD=1 selects the scalar full-Walsh kernel.
 void fine_apply_f64(const FineOp& op, const double* u, double* y, cudaStream_t s) {
-  if (op.walsh_ok) fine_apply_walsh_f64(op, u, y, s);
+  static const bool old = getenv("SG_WALSH64_OLD") != nullptr;
+  if (!old && p64_supported(op)) fine_apply_p64(op, u, y, s);
+  else if (op.walsh_ok) fine_apply_walsh_f64(op, u, y, s);
   else fine_apply_dense_f64(op, u, y, s);
 }
 // FP32 on node-layout vectors: converted through the P32 layout and the

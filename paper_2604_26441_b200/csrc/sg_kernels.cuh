@@ -76,6 +76,8 @@ void stencil_sym64(const Grid& g, const double* Ts, int mode, const double* x, d
 void stencil_res64(const Grid& g, const double* At, const double* x, const double* r, double* out,
                    cudaStream_t s);
 int kKwColHost(int q);
+bool p64_supported(const FineOp& op);
+void fine_apply_p64(const FineOp& op, const double* u, double* y, cudaStream_t s);
 void make_state_device(int kind, int nx, int ny, int nz, double vf, double floor_,
                        unsigned long long seed, double* rho, cudaStream_t s);
 void fine_apply_dense_f32(const FineOp& op, const float* u, float* y, cudaStream_t s);

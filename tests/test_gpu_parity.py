@@ -290,6 +290,32 @@ def test_fine_apply_fp32_packed_tiling(dims, kind):
     assert np.array_equal(y, op.matvec_tagged(u32, P.PrecisionTag.FP32))
 
 
+@pytest.mark.parametrize("dims,kind", [((100, 100, 100), "uniform"), ((131, 7, 5), "binary"),
+                                       ((9, 33, 17), "random_floor"), ((1, 1, 1), "uniform"),
+                                       ((2, 61, 3), "binary"), ((200, 3, 2), "binary"),
+                                       ((257, 2, 3), "random_floor"), ((63, 40, 9), "binary")])
+def test_fine_apply_fp64_block_tiling(dims, kind):
+    """FP64 apply (block-form, plane-shared Walsh kernel, sg_fine_p64.cu) across
+    tile shapes -- x tiles, odd sizes, one element -- and configs[3] at full size."""
+    g, op, og, E, ke = _pair(dims, kind)
+    u = P.SplitMix64(5).gaussian(g.n_free)
+    y = op.matvec_tagged(u, P.PrecisionTag.FP64)
+    assert _rel(y, O.fine_apply(og, E, ke, u, "fp64")) < 1e-13
+    assert np.array_equal(y, op.matvec_tagged(u, P.PrecisionTag.FP64))
+
+
+def test_fine_apply_fp64_general_mask():
+    nx, ny, nz = 14, 9, 6
+    rng = np.random.default_rng(4)
+    mask = rng.random(3 * (nx + 1) * (ny + 1) * (nz + 1)) < 0.2
+    g = P.make_grid(nx, ny, nz, mask)
+    op = P.FineOperator(g, P.simp_modulus(P.make_state("binary", nx, ny, nz, vf=0.5, seed=42), 3.0))
+    og = O.make_grid(nx, ny, nz, mask)
+    u = P.SplitMix64(9).gaussian(g.n_free)
+    assert _rel(op.matvec_tagged(u, P.PrecisionTag.FP64),
+                O.fine_apply(og, op.modulus.E, op.ke, u, "fp64")) < 1e-13
+
+
 def test_fine_apply_fp32_general_mask():
     """Non-cantilever Dirichlet mask (per-DOF, grid.py make_grid) on the packed kernel."""
     nx, ny, nz = 14, 9, 6
