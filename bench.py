@@ -183,8 +183,9 @@ def _config(args):
     N = args.size
     return {"workload": f"{N}x{N}x{N} uniform rho=0.5 p=3 cantilever, FP32-GMG PCG (tol 1e-6, cap 200)",
             "elements": N ** 3, "levels_requested": 4, "policy": "fp32",
-            "parallelism": (f"z-slab partition x{args.gpus} (levels 0-1; NCCL halos + rank-ordered "
-                            "dot sums; coarse tail replicated)") if (args.gpus > 1 or args.slab) else "single GPU",
+            "parallelism": (f"z-slab partition x{args.gpus} (levels 0-1; {args.transport} transport: "
+                            + ("device kernels over CUDA IPC mailboxes, " if args.transport == "peer" else "NCCL via torch.distributed, ")
+                            + "halos + rank-ordered dot sums; coarse tail replicated)") if (args.gpus > 1 or args.slab) else "single GPU",
             "l2": "working set > 126 MB L2 (level-1 operator 258 MB, its symmetric copy 133 MB); L2 also flushed before each timed solve"}
 
 
@@ -227,11 +228,47 @@ def run_gpu(args):
     cfg = P.SolverConfig(tol=1e-6, maxiter=200)
     flush = torch.empty(256 * 2 ** 20 // 4, dtype=torch.float32, device="cuda")
     stream = torch.cuda.current_stream()
+    # per-component device timings (CUDA events inside the library), taken
+    # before a slab solver may release the hierarchy's replicated levels
+    def prof(what, reps=10):
+        out = ctypes.c_double()
+        _native.check(lib.sg_hier_profile(h._hh, what, reps, ctypes.byref(out), _dev.stream()))
+        return out.value
+
+    n_free, n_elem = g.n_free, g.n_elem
+    nn1 = (N // 2 + 1) ** 3
+    comps = {}
+    t32 = prof(0)
+    t64 = prof(1)
+    tl1 = prof(2)
+    tco = prof(3)
+    tvc = prof(4)
+    tbf = prof(5)
+    try:
+        tch = prof(6)
+    except Exception:
+        tch = None
+    peak, peak_kind = _peaks()
+    b32 = 8 * n_free + 4 * n_elem
+    b64 = 16 * n_free + 8 * n_elem
+    # level-1 SpMV on the symmetric stencil copy (126 of 243 coefficients per
+    # node from HBM; SG_ST64_FULL=1 selects the full 243)
+    bl1 = ((243 if os.environ.get("SG_ST64_FULL") else 126) * 8 + 48) * nn1
+    comps["fine_apply_fp32"] = {"ms": t32, "alg_bytes": b32, "gbs": b32 / t32 / 1e6}
+    comps["fine_apply_fp64"] = {"ms": t64, "alg_bytes": b64, "gbs": b64 / t64 / 1e6}
+    comps["fine_apply_bf16_tcgen05"] = {"ms": tbf, "alg_bytes": b32, "gbs": b32 / tbf / 1e6}
+    if tch is not None:
+        # fused apply + Chebyshev step: u, E in; b, dinv, d in; d, x' out (FP32)
+        bch = 24 * n_free + 4 * n_elem
+        comps["fine_apply_cheb_fused_fp32"] = {"ms": tch, "alg_bytes": bch, "gbs": bch / tch / 1e6}
+    comps["level1_spmv_fp64"] = {"ms": tl1, "alg_bytes": bl1, "gbs": bl1 / tl1 / 1e6}
+    comps["coarsest_pcg80"] = {"ms": tco}
+    comps["vcycle"] = {"ms": tvc}
     if use_slab:
         # slab partition of levels 0-1 over the ranks (NCCL halos / dot sums),
         # coarse tail replicated (paper_2604_26441_b200/slab.py)
         from paper_2604_26441_b200.slab import SlabSolver
-        slab = SlabSolver(op, h)
+        slab = SlabSolver(op, h, transport=args.transport, release_full=True)
         solve = lambda b: slab.pcg(b, cfg)
     else:
         solve = lambda b: P.pcg(op.matvec, h.vcycle, b, cfg)
@@ -322,41 +359,6 @@ def run_gpu(args):
                   "numpy_note": "reference calling convention: numpy b in, numpy x out "
                                 "(pageable H2D/D2H inside P.pcg)"}
 
-    # per-component device timings (CUDA events inside the library)
-    def prof(what, reps=10):
-        out = ctypes.c_double()
-        _native.check(lib.sg_hier_profile(h._hh, what, reps, ctypes.byref(out), _dev.stream()))
-        return out.value
-
-    n_free, n_elem = g.n_free, g.n_elem
-    nn1 = (N // 2 + 1) ** 3
-    comps = {}
-    t32 = prof(0)
-    t64 = prof(1)
-    tl1 = prof(2)
-    tco = prof(3)
-    tvc = prof(4)
-    tbf = prof(5)
-    try:
-        tch = prof(6)
-    except Exception:
-        tch = None
-    peak, peak_kind = _peaks()
-    b32 = 8 * n_free + 4 * n_elem
-    b64 = 16 * n_free + 8 * n_elem
-    # level-1 SpMV on the symmetric stencil copy (126 of 243 coefficients per
-    # node from HBM; SG_ST64_FULL=1 selects the full 243)
-    bl1 = ((243 if os.environ.get("SG_ST64_FULL") else 126) * 8 + 48) * nn1
-    comps["fine_apply_fp32"] = {"ms": t32, "alg_bytes": b32, "gbs": b32 / t32 / 1e6}
-    comps["fine_apply_fp64"] = {"ms": t64, "alg_bytes": b64, "gbs": b64 / t64 / 1e6}
-    comps["fine_apply_bf16_tcgen05"] = {"ms": tbf, "alg_bytes": b32, "gbs": b32 / tbf / 1e6}
-    if tch is not None:
-        # fused apply + Chebyshev step: u, E in; b, dinv, d in; d, x' out (FP32)
-        bch = 24 * n_free + 4 * n_elem
-        comps["fine_apply_cheb_fused_fp32"] = {"ms": tch, "alg_bytes": bch, "gbs": bch / tch / 1e6}
-    comps["level1_spmv_fp64"] = {"ms": tl1, "alg_bytes": bl1, "gbs": bl1 / tl1 / 1e6}
-    comps["coarsest_pcg80"] = {"ms": tco}
-    comps["vcycle"] = {"ms": tvc}
     achieved = b32 / (t32 * 1e-3) / 1e9
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
@@ -407,6 +409,8 @@ def main():
     ap.add_argument("--size", type=int, default=100)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--slab", action="store_true", help="use the slab-partitioned path even on 1 GPU")
+    ap.add_argument("--transport", default="peer", choices=["peer", "torch"],
+                    help="slab transport: device kernels over CUDA IPC (peer) or torch.distributed")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)

@@ -220,6 +220,23 @@ typedef struct sg_dist sg_dist;
 int sg_dist_create(sg_hier* h, int n_dist, const int32_t* planes, const sg_comm* comm,
                    void* stream, sg_dist** out);
 void sg_dist_destroy(sg_dist* d);
+/* Same slab handle on the DEVICE transport (sg_peer.cu): halos, rank-ordered
+ * sums and allgathers are kernels that store into the peer ranks' mailboxes
+ * (CUDA IPC mappings) and signal with system-scope release/acquire flags; no
+ * host callback, and the distributed cycle is captured in a CUDA graph.
+ * planes_all: world x n_dist x {w0, w1, o0, o1} (every rank's windows).
+ * Replaces the host-callback transport (slab.py TorchSlabComm) of sg_dist_create. */
+int sg_dist_create_peer(sg_hier* h, int n_dist, const int32_t* planes_all, int rank, int world,
+                        void* stream, sg_dist** out);
+/* This rank's mailbox: 64-byte cudaIpcMemHandle_t (handle_out may be NULL) and
+ * its device address (for ranks sharing one process; base_out may be NULL). */
+int sg_dist_peer_handle(sg_dist* d, void* handle_out, uint64_t* base_out);
+/* Map every other rank's mailbox: handles = world x 64 bytes (IPC, other
+ * processes) or bases = world device addresses (same process); one is NULL. */
+int sg_dist_peer_open(sg_dist* d, const void* handles, const uint64_t* bases);
+/* Free the replicated full-grid copies of the slab levels held by the
+ * hierarchy (its single-GPU cycle then reports an error). */
+int sg_dist_release_full(sg_dist* d, void* stream);
 /* method 0 = pcg (krylov.py:113-165), 1 = fgmres (krylov.py:168-281), with
  * apply_K = op.matvec under ktag and apply_M = V (gamma 1) / W (gamma 2) cycle. */
 int sg_dist_solve(sg_dist* d, int method, int ktag, int gamma, const double* b_free,
@@ -268,6 +285,10 @@ int sg_make_state(int kind, int nx, int ny, int nz, double vf, double floor_, ui
  *   planes per z chunk, z chunks}.
  * ------------------------------------------------------------------- */
 int sg_plan_brick(int nx, int ny, int nz, int nsm, int32_t* out3);
+/* slab.py halo_pieces restated natively (sg_peer.cu): windows = world x
+ * {w0, w1, o0, o1} of one level -> out = {src, dst, p0, p1} pieces, -1
+ * terminated (cap = max pieces). */
+int sg_plan_halo(int world, const int32_t* windows, int32_t* out, int cap);
 int sg_plan_p32(int nx, int ny, int nz, int nsm, int32_t* out7);
 
 #ifdef __cplusplus

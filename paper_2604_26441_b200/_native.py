@@ -107,6 +107,12 @@ SIGNATURES = {
                            P(c_int), c_void_p]),
     "sg_dist_create": (c_int, [c_void_p, c_int, c_void_p, P(Comm), c_void_p, P(c_void_p)]),
     "sg_dist_destroy": (None, [c_void_p]),
+    "sg_dist_create_peer": (c_int, [c_void_p, c_int, c_void_p, c_int, c_int, c_void_p,
+                                    P(c_void_p)]),
+    "sg_dist_peer_handle": (c_int, [c_void_p, c_void_p, P(c_u64)]),
+    "sg_dist_peer_open": (c_int, [c_void_p, c_void_p, c_void_p]),
+    "sg_dist_release_full": (c_int, [c_void_p, c_void_p]),
+    "sg_plan_halo": (c_int, [c_int, c_void_p, c_void_p, c_int]),
     "sg_dist_solve": (c_int, [c_void_p, c_int, c_int, c_int, c_void_p, c_void_p, P(SolverCfg),
                               P(Report), c_void_p, c_void_p]),
     "sg_dist_apply": (c_int, [c_void_p, c_int, c_int, c_int, c_void_p, c_void_p, c_void_p]),

@@ -43,6 +43,7 @@ int guard(F&& f) {
 inline cudaStream_t S(void* p) { return reinterpret_cast<cudaStream_t>(p); }
 
 sg::Level& level_of(sg_hier* h, int level) {
+  SG_REQUIRE(!h->h->released, "hierarchy levels were released to a slab solver");
   SG_REQUIRE(level >= 0 && level < int(h->h->lv.size()), "level index out of range");
   return *h->h->lv[size_t(level)];
 }
@@ -243,6 +244,7 @@ int sg_hier_level_diag(sg_hier* h, int level, double* d, void* stream) {
 int sg_hier_cycle(sg_hier* h, int gamma, const double* r, double* z, void* stream) {
   return guard([&] {
     std::lock_guard<std::mutex> lk(h->mu);
+    SG_REQUIRE(!h->h->released, "hierarchy levels were released to a slab solver (single-GPU cycle unavailable)");
     cudaStream_t s = S(stream);
     sg::Level& L0 = *h->h->lv[0];
     sg::scatter_free<double>(*L0.g, r, L0.w.r.p, s);
@@ -350,6 +352,7 @@ static int run_solver(int which, sg_fine* f, int ktag, sg_hier* h, int gamma, co
     std::unique_lock<std::mutex> lh;
     if (h) {
       SG_REQUIRE(h->fine == f, "hierarchy built for a different operator");
+      SG_REQUIRE(!h->h->released, "hierarchy levels were released to a slab solver");
       lh = std::unique_lock<std::mutex>(h->mu);
     }
     cudaStream_t s = S(stream);
@@ -392,6 +395,7 @@ int sg_dist_create(sg_hier* h, int n_dist, const int32_t* planes, const sg_comm*
   return guard([&] {
     SG_REQUIRE(h && planes && comm && out && comm->halo && comm->allreduce && comm->allgather,
                "null argument");
+    SG_REQUIRE(!h->h->released, "hierarchy levels were released to a slab solver");
     std::lock_guard<std::mutex> lk(h->mu);
     sg::CommHooks c;
     c.ctx = comm->ctx;
@@ -403,6 +407,76 @@ int sg_dist_create(sg_hier* h, int n_dist, const int32_t* planes, const sg_comm*
     d->hier = h;
     d->d = sg::dist_build(*h->h, n_dist, pl.data(), c, S(stream));
     *out = d.release();
+  });
+}
+
+int sg_dist_create_peer(sg_hier* h, int n_dist, const int32_t* planes_all, int rank, int world,
+                        void* stream, sg_dist** out) {
+  return guard([&] {
+    SG_REQUIRE(h && planes_all && out && world >= 1 && rank >= 0 && rank < world, "bad argument");
+    SG_REQUIRE(n_dist >= 1 && n_dist <= 2 && int(h->h->lv.size()) > n_dist, "1 or 2 slab levels");
+    SG_REQUIRE(!h->h->released, "hierarchy levels were released to a slab solver");
+    std::lock_guard<std::mutex> lk(h->mu);
+    cudaStream_t s = S(stream);
+    int64_t pnd[2] = {0, 0};
+    int fpl[2] = {0, 0};
+    for (int l = 0; l < n_dist; ++l) {
+      const sg::GridDesc& g = h->h->lv[size_t(l)]->g->d;
+      pnd[l] = 3 * int64_t(g.nx + 1) * (g.ny + 1);
+      fpl[l] = g.nz + 1;
+    }
+    // level 0 in the P32 layout (FP32 level-0 smoother) exchanges its own planes
+    const sg::Level& L0 = *h->h->lv[0];
+    const int64_t p32_plane = L0.p32 ? 3 * int64_t(sg::p32_xs(L0.g->d)) * (L0.g->d.ny + 1) : 0;
+    sg::CommHooks c;
+    sg::PeerComm* pc = sg::peer_create(rank, world, n_dist, planes_all, pnd, fpl, p32_plane, s, c);
+    std::vector<int> pl(planes_all + size_t(rank) * n_dist * 4, planes_all + size_t(rank + 1) * n_dist * 4);
+    auto d = std::make_unique<sg_dist>();
+    d->hier = h;
+    try {
+      d->d = sg::dist_build(*h->h, n_dist, pl.data(), c, s);
+    } catch (...) {
+      sg::peer_destroy(pc);
+      throw;
+    }
+    d->d->peer = pc;
+    *out = d.release();
+  });
+}
+
+int sg_dist_peer_handle(sg_dist* d, void* handle_out, uint64_t* base_out) {
+  return guard([&] {
+    SG_REQUIRE(d && d->d->peer, "not a device-transport slab handle");
+    if (handle_out) sg::peer_handle(d->d->peer, handle_out);
+    if (base_out) *base_out = sg::peer_base(d->d->peer);
+  });
+}
+
+int sg_dist_peer_open(sg_dist* d, const void* handles, const uint64_t* bases) {
+  return guard([&] {
+    SG_REQUIRE(d && d->d->peer && (handles || bases), "bad argument");
+    sg::peer_open(d->d->peer, handles, reinterpret_cast<const unsigned long long*>(bases));
+  });
+}
+
+int sg_dist_release_full(sg_dist* d, void* stream) {
+  return guard([&] {
+    SG_REQUIRE(d, "null argument");
+    std::lock_guard<std::mutex> lk(d->hier->mu);
+    sg::dist_release_full(*d->d, S(stream));
+  });
+}
+
+int sg_plan_halo(int world, const int32_t* windows, int32_t* out, int cap) {
+  return guard([&] {
+    std::vector<std::array<int, 4>> w(static_cast<size_t>(world));
+    for (int r = 0; r < world; ++r)
+      for (int k = 0; k < 4; ++k) w[size_t(r)][size_t(k)] = windows[4 * r + k];
+    const auto pcs = sg::halo_pieces(w);
+    SG_REQUIRE(int(pcs.size()) <= cap, "piece buffer too small");
+    for (size_t i = 0; i < pcs.size(); ++i)
+      for (int k = 0; k < 4; ++k) out[4 * i + size_t(k)] = pcs[i][size_t(k)];
+    out[4 * pcs.size()] = -1;
   });
 }
 

@@ -23,9 +23,11 @@ struct Error : std::runtime_error {
 #define SG_CUDA(call)                                                              \
   do {                                                                             \
     cudaError_t _e = (call);                                                       \
-    if (_e != cudaSuccess)                                                         \
+    if (_e != cudaSuccess) {                                                       \
+      (void)cudaGetLastError(); /* a non-sticky API error must not resurface */    \
       throw ::sg::Error(std::string("CUDA error ") + cudaGetErrorString(_e) +     \
                         " at " __FILE__ ":" + std::to_string(__LINE__));           \
+    }                                                                              \
   } while (0)
 
 // Every kernel launch of the library is followed by SG_CHECK_LAUNCH(), which

@@ -117,7 +117,7 @@ void level_apply(Hier& H, Level& L, int tag, const void* x, void* y, cudaStream_
     fine_apply_tag(*H.fine, tag, x, y, s);
     return;
   }
-  if (tag == TAG_FP64 && L.st.T64s.p && !H.comm) {
+  if (tag == TAG_FP64 && L.st.T64s.p) {
     stencil_sym64(*L.g, L.st.T64s.p, 0, (const double*)x, (double*)y, nullptr, nullptr, nullptr, 0.0, 0.0,
                   true, s);
   } else if (tag == TAG_FP64) {
@@ -219,6 +219,10 @@ static void smooth_p32(Hier& H, Level& L, const double* b64, const double* x0, d
   const float* dinv = L.dinv32p.p;
   static const bool unfused = std::getenv("SG_P32_UNFUSED") != nullptr;  // A/B check
   bool out_done = false;
+  // slab window: ghost planes of the iterate before every apply
+  auto halo = [&](const float* v) {
+    if (H.comm) H.comm->exchange(kP32Level, v, 4, s);
+  };
   if (L.kind == 0) {  // Chebyshev
     const double lam = L.lam;
     const double sigma = 0.5 * (lam + L.alpha * lam);
@@ -230,6 +234,7 @@ static void smooth_p32(Hier& H, Level& L, const double* b64, const double* x0, d
     } else {
       if (!b_ready) to_p32<double>(g, b64, b, s);
       if (!x0_ready) to_p32<double>(g, x0, x, s);
+      halo(x);
       if (unfused) {
         fine_apply_p32(op, x, L.w.y32.p, s);
         launch_ew(n, s, [&](int nb, int nt) { cheb_first_kernel<float><<<nb, nt, 0, s>>>(n, dinv, b, L.w.y32.p, c0, d, x); });
@@ -243,6 +248,7 @@ static void smooth_p32(Hier& H, Level& L, const double* b64, const double* x0, d
     for (int it = 1; it < L.degree; ++it) {
       const double c = delta * delta * a / 4.0;
       a = 1.0 / (sigma - c);
+      halo(x);
       if (unfused) {
         fine_apply_p32(op, x, L.w.y32.p, s);
         const float A = float(a), AC = float(a * c);
@@ -265,6 +271,7 @@ static void smooth_p32(Hier& H, Level& L, const double* b64, const double* x0, d
       to_p32<double>(g, x0, x, s);
     }
     for (int it = 0; it < steps; ++it) {
+      halo(x);
       fine_apply_p32(op, x, L.w.y32.p, s);
       launch_ew(n, s, [&](int nb, int nt) { jac_step_kernel<float><<<nb, nt, 0, s>>>(n, dinv, b, L.w.y32.p, w, x); });
     }
@@ -294,7 +301,10 @@ static void res64(Level& L, const double* x, const double* r, double* out, cudaS
 // the last lands in `out` and no step reads the buffer it writes.
 static bool smooth_st64(Hier& H, Level& L, const double* b, const double* x0, double* out,
                         cudaStream_t s) {
-  if (L.is_fine || L.kind != 0 || H.comm || std::getenv("SG_ST64_UNFUSED")) return false;
+  if (L.is_fine || L.kind != 0 || std::getenv("SG_ST64_UNFUSED")) return false;
+  auto halo = [&](const double* v) {  // slab window: ghost planes before every apply
+    if (H.comm) H.comm->exchange(L.idx, v, 8, s);
+  };
   const int64_t n = L.nd();
   const double lam = L.lam;
   const double sigma = 0.5 * (lam + L.alpha * lam);
@@ -311,6 +321,7 @@ static bool smooth_st64(Hier& H, Level& L, const double* b, const double* x0, do
     launch_ew(n, s, [&](int nb, int nt) { cheb_first0_kernel<double><<<nb, nt, 0, s>>>(n, L.dinv.p, b, c0, d, x1); });
     cur = x1;
   } else {
+    halo(x0);
     cheb64(L, x0, buf(1), b, d, c0, 0.0, true, s);
     cur = buf(1);
   }
@@ -318,6 +329,7 @@ static bool smooth_st64(Hier& H, Level& L, const double* b, const double* x0, do
   for (int it = 1; it < D; ++it) {
     const double c = delta * delta * a / 4.0;
     a = 1.0 / (sigma - c);
+    halo(cur);
     cheb64(L, cur, buf(it + 1), b, d, a, a * c, false, s);
     cur = buf(it + 1);
   }
@@ -346,19 +358,25 @@ void coarsest_solve(Hier& H, const double* r, double* x, cudaStream_t s) {
 }
 
 // hierarchy.py:207-216
+static void dist_tail(DistPart& D, int l, int gamma, double* x64, cudaStream_t s);
+
+// On a slab window hierarchy (H.comm / H.dist set) the same recursion runs on
+// the windows: every operator input is halo-exchanged first, and below the
+// last slab level the replicated coarse tail takes over (dist_tail).
 void cycle(Hier& H, int l, int gamma, cudaStream_t s) {
   Level& L = *H.lv[size_t(l)];
-  if (l == int(H.lv.size()) - 1) {
+  if (l == int(H.lv.size()) - 1 && !H.dist) {
     coarsest_solve(H, L.w.r.p, L.w.x.p, s);
     return;
   }
-  Level& C = *H.lv[size_t(l + 1)];
+  Level* Cp = l + 1 < int(H.lv.size()) ? H.lv[size_t(l + 1)].get() : nullptr;
   const int64_t n = L.nd();
   // pre-smoothing writes x (f64) into w.d64 scratch first, then moved to w.x
   double* x64 = L.w.d64.p;  // holds the f64 iterate across the coarse visits
   level_smooth(H, l, L.w.r.p, nullptr, x64, s);
   for (int g = 0; g < gamma; ++g) {
-    if (L.tag == TAG_FP64 && !L.is_fine && !H.comm && !std::getenv("SG_ST64_UNFUSED")) {
+    if (L.tag == TAG_FP64 && !L.is_fine && !std::getenv("SG_ST64_UNFUSED")) {
+      if (H.comm) H.comm->exchange(l, x64, 8, s);
       res64(L, x64, L.w.r.p, L.w.x.p, s);  // r - A x in one pass
     } else if (L.tag == TAG_FP64) {
       level_apply(H, L, TAG_FP64, x64, L.w.y64.p, s);
@@ -371,18 +389,27 @@ void cycle(Hier& H, int l, int gamma, cudaStream_t s) {
       if (!xc) {  // W-cycle second pass: x32 = f32(x64) was written by prolong
         xc = L.w.x32.p;
       }
+      if (H.comm) H.comm->exchange(kP32Level, xc, 4, s);
       fine_apply_p32_res(*H.fine, xc, L.w.r.p, L.w.x.p, s);
     } else {
       cvt_f64_to_f32(n, x64, L.w.x32.p, s);
       level_apply(H, L, L.tag, L.w.x32.p, L.w.y32.p, s);
       launch_ew(n, s, [&](int nb, int nt) { residual_kernel<float><<<nb, nt, 0, s>>>(n, L.w.r.p, L.w.y32.p, L.w.x.p); });
     }
-    restrict_(*L.g, *C.g, L.w.x.p, C.w.r.p, s);  // L.w.x used as residual scratch here
-    cycle(H, l + 1, gamma, s);
-    if (L.p32)  // also writes f32(x64) into x32 (P32) for the post-smoother
-      prolong(*L.g, *C.g, C.w.x.p, x64, /*add=*/true, s, L.w.x32.p, p32_xs(L.g->d));
-    else
-      prolong(*L.g, *C.g, C.w.x.p, x64, /*add=*/true, s);
+    if (H.comm) H.comm->exchange(l, L.w.x.p, 8, s);  // restriction reads ghost residuals
+    if (H.dist && l + 1 == H.dist->n_dist) {
+      dist_tail(*H.dist, l, gamma, x64, s);
+      if (L.p32) to_p32<double>(L.g->d, x64, L.w.x32.p, s);  // f32(x64) for the post-smoother
+    } else {
+      Level& C = *Cp;
+      restrict_(*L.g, *C.g, L.w.x.p, C.w.r.p, s);  // L.w.x used as residual scratch here
+      cycle(H, l + 1, gamma, s);
+      if (H.comm) H.comm->exchange(l + 1, C.w.x.p, 8, s);  // prolongation reads ghost corrections
+      if (L.p32)  // also writes f32(x64) into x32 (P32) for the post-smoother
+        prolong(*L.g, *C.g, C.w.x.p, x64, /*add=*/true, s, L.w.x32.p, p32_xs(L.g->d));
+      else
+        prolong(*L.g, *C.g, C.w.x.p, x64, /*add=*/true, s);
+    }
     L.w.xcur = nullptr;  // x64 changed: a W-cycle's next residual re-converts
   }
   if (L.p32) {
@@ -398,6 +425,7 @@ Hier::~Hier() {
 }
 
 void cycle_run(Hier& H, int gamma, cudaStream_t s) {
+  SG_REQUIRE(!H.released, "hierarchy levels were released to a slab solver (single-GPU cycle unavailable)");
   static const bool no_graph = [] {
     const char* e = std::getenv("SG_NO_GRAPH");
     return e && e[0] == '1';
@@ -644,46 +672,102 @@ std::unique_ptr<Hier> hier_build(FineOp* fine, FineWork& fw, const HParams& p, c
 // cut level the residual is allgathered into the replicated full hierarchy,
 // the coarse tail runs there, and the prolonged correction (P x_c formed
 // first, then added: the bits of prolong(add=true)) is sliced back.
-static void dist_level(DistPart& D, int l, int gamma, cudaStream_t s) {
-  Hier& W = *D.W;
+// Below the last slab level: the owned planes of the residual are
+// allgathered into the replicated full hierarchy, the coarse tail runs there,
+// and the prolonged correction (P x_c formed first, then added: the bits of
+// prolong(add=true)) is sliced back into the window iterate x64.
+static void dist_tail(DistPart& D, int l, int gamma, double* x64, cudaStream_t s) {
   Hier& F = *D.full;
-  Level& L = *W.lv[size_t(l)];
+  Level& L = *D.W->lv[size_t(l)];
+  Level& FL = *F.lv[size_t(l)];
+  Level& FC = *F.lv[size_t(l + 1)];
   const int64_t n = L.nd();
-  double* x64 = L.w.d64.p;
-  level_smooth(W, l, L.w.r.p, nullptr, x64, s);
-  for (int g = 0; g < gamma; ++g) {
-    if (L.tag == TAG_FP64) {
-      level_apply(W, L, TAG_FP64, x64, L.w.y64.p, s);
-      launch_ew(n, s, [&](int nb, int nt) { residual_kernel<double><<<nb, nt, 0, s>>>(n, L.w.r.p, L.w.y64.p, L.w.x.p); });
-    } else {
-      cvt_f64_to_f32(n, x64, L.w.x32.p, s);
-      level_apply(W, L, L.tag, L.w.x32.p, L.w.y32.p, s);
-      launch_ew(n, s, [&](int nb, int nt) { residual_kernel<float><<<nb, nt, 0, s>>>(n, L.w.r.p, L.w.y32.p, L.w.x.p); });
-    }
-    if (l + 1 < D.n_dist) {
-      Level& C = *W.lv[size_t(l + 1)];
-      D.comm.exchange(l, L.w.x.p, 8, s);
-      restrict_(*L.g, *C.g, L.w.x.p, C.w.r.p, s);
-      dist_level(D, l + 1, gamma, s);
-      D.comm.exchange(l + 1, C.w.x.p, 8, s);
-      prolong(*L.g, *C.g, C.w.x.p, x64, /*add=*/true, s);
-    } else {
-      Level& FL = *F.lv[size_t(l)];
-      Level& FC = *F.lv[size_t(l + 1)];
-      D.comm.gather(l, L.w.x.p, FL.w.x.p, s);
-      restrict_(*FL.g, *FC.g, FL.w.x.p, FC.w.r.p, s);
-      cycle(F, l + 1, gamma, s);
-      prolong(*FL.g, *FC.g, FC.w.x.p, FL.w.y64.p, /*add=*/false, s);
-      const double* slice = FL.w.y64.p + int64_t(D.w0[l]) * D.plane_nd(l);
-      launch_ew(n, s, [&](int nb, int nt) { add_kernel<<<nb, nt, 0, s>>>(n, slice, x64); });
-    }
-  }
-  level_smooth(W, l, L.w.r.p, x64, L.w.x.p, s);
+  D.comm.gather(l, L.w.x.p, FL.w.x.p, s);
+  restrict_(*FL.g, *FC.g, FL.w.x.p, FC.w.r.p, s);
+  cycle(F, l + 1, gamma, s);
+  prolong(*FL.g, *FC.g, FC.w.x.p, FL.w.y64.p, /*add=*/false, s);
+  const double* slice = FL.w.y64.p + int64_t(D.w0[l]) * D.plane_nd(l);
+  launch_ew(n, s, [&](int nb, int nt) { add_kernel<<<nb, nt, 0, s>>>(n, slice, x64); });
 }
 
 void dist_cycle(DistPart& D, int gamma, cudaStream_t s) {
   SG_REQUIRE(gamma == 1 || gamma == 2, "gamma must be 1 (V) or 2 (W)");
-  dist_level(D, 0, gamma, s);
+  cycle(*D.W, 0, gamma, s);
+}
+
+DistPart::~DistPart() {
+  for (auto& g : graph)
+    if (g) cudaGraphExecDestroy(g);
+  if (peer) peer_destroy(peer);
+}
+
+// Device transport: no host step inside the cycle, so it is captured once and
+// replayed like the single-GPU cycle (cycle_run); host hooks run eagerly.
+void dist_cycle_run(DistPart& D, int gamma, cudaStream_t s) {
+  static const bool no_graph = [] {
+    const char* e = std::getenv("SG_NO_GRAPH");
+    return e && e[0] == '1';
+  }();
+  SG_REQUIRE(gamma == 1 || gamma == 2, "gamma must be 1 (V) or 2 (W)");
+  if (no_graph || !D.peer) {
+    dist_cycle(D, gamma, s);
+    return;
+  }
+  if (!D.graph[gamma]) {
+    cudaStream_t cs = nullptr;
+    SG_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+    cudaGraph_t g = nullptr;
+    SG_CUDA(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+    try {
+      dist_cycle(D, gamma, cs);
+    } catch (...) {
+      cudaStreamEndCapture(cs, &g);
+      if (g) cudaGraphDestroy(g);
+      cudaStreamDestroy(cs);
+      throw;
+    }
+    SG_CUDA(cudaStreamEndCapture(cs, &g));
+    cudaStreamDestroy(cs);
+    size_t n = 0;
+    SG_CUDA(cudaGraphGetNodes(g, nullptr, &n));
+    SG_CUDA(cudaGraphInstantiate(&D.graph[gamma], g, 0));
+    SG_CUDA(cudaGraphDestroy(g));
+    D.graph_nodes[gamma] = n;
+  }
+  SG_CUDA(cudaGraphLaunch(D.graph[gamma], s));
+  __atomic_add_fetch(&g_sg_launches, (unsigned long long)D.graph_nodes[gamma], __ATOMIC_RELAXED);
+}
+
+void dist_release_full(DistPart& D, cudaStream_t s) {
+  SG_CUDA(cudaStreamSynchronize(s));
+  Hier& F = *D.full;
+  for (int l = 0; l < D.n_dist; ++l) {
+    Level& L = *F.lv[size_t(l)];
+    const bool cut = l == D.n_dist - 1;
+    L.st = Stencil{};
+    L.diag.release();
+    L.dinv.release();
+    L.dinv32.release();
+    L.dinv32p.release();
+    L.w.r.release();
+    L.w.d64.release();
+    L.w.dd64.release();
+    for (auto* b : {&L.w.b32, &L.w.x32, &L.w.y32, &L.w.dd32, &L.w.x32b}) b->release();
+    L.w.xcur = nullptr;
+    if (!cut) {
+      L.w.x.release();
+      L.w.y64.release();
+    }
+  }
+  for (auto& g : F.graph)
+    if (g) {
+      cudaGraphExecDestroy(g);
+      g = nullptr;
+    }
+  F.io_a.release();
+  F.io_b.release();
+  D.full_released = true;
+  F.released = true;
 }
 
 template <class T>
@@ -761,6 +845,7 @@ std::unique_ptr<DistPart> dist_build(Hier& F, int n_dist, const int* planes, con
     if (l == 0) {
       L->is_fine = true;
       L->g = &wf.grid;
+      L->p32 = FL.p32 && p32_supported(wf);  // same FP32 level-0 kernels as one GPU
     } else {
       build_window_grid(*FL.g, D->w0[l], D->w1[l], L->own, s);
       L->g = &L->own;
@@ -774,6 +859,9 @@ std::unique_ptr<DistPart> dist_build(Hier& F, int n_dist, const int* planes, con
         stencil_tile<float>(L->own, L->st.A32.p, L->st.T32, s);
       }
       stencil_tile<double>(L->own, L->st.A64.p, L->st.T64, s);
+      // the symmetric copy when the full hierarchy has one: owned rows read
+      // their lower blocks from neighbours inside the window (ghost planes)
+      if (FL.st.T64s.p) stencil_sym_tile(L->own, L->st.A64.p, L->st.T64s, s);
     }
     const int64_t n = 3 * L->g->d.nnodes();
     const int64_t voff = int64_t(D->w0[l]) * 3 * (FL.g->d.nx + 1) * (FL.g->d.ny + 1);
@@ -783,11 +871,16 @@ std::unique_ptr<DistPart> dist_build(Hier& F, int n_dist, const int* planes, con
     SG_CUDA(cudaMemcpyAsync(L->diag.p, FL.diag.p + voff, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
     SG_CUDA(cudaMemcpyAsync(L->dinv.p, FL.dinv.p + voff, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
     SG_CUDA(cudaMemcpyAsync(L->dinv32.p, FL.dinv32.p + voff, sizeof(float) * n, cudaMemcpyDeviceToDevice, s));
+    if (L->p32) {
+      L->dinv32p.alloc(size_t(L->n32()));
+      to_p32<float>(L->g->d, L->dinv32.p, L->dinv32p.p, s);
+    }
     alloc_work(*L, s);
     for (auto* b : {&L->w.r, &L->w.x, &L->w.d64, &L->w.y64, &L->w.dd64}) b->zero(s);
-    for (auto* b : {&L->w.b32, &L->w.x32, &L->w.y32, &L->w.dd32}) b->zero(s);
+    for (auto* b : {&L->w.b32, &L->w.x32, &L->w.y32, &L->w.dd32, &L->w.x32b}) b->zero(s);
     W->lv.push_back(std::move(L));
   }
+  W->dist = D.get();
   D->W = std::move(W);
   // flat-Jacobi scratch of the window operator (1/diag of level 0)
   D->wfw.dinv.alloc(size_t(D->W->lv[0]->nd()));

@@ -1,6 +1,8 @@
 // Hierarchy, cycle and solver orchestration (host C++ driving device kernels).
 #pragma once
+#include <array>
 #include <memory>
+#include <vector>
 #include "sg_coarse.cuh"
 
 namespace sg {
@@ -21,6 +23,10 @@ struct HParams {
 // Host callbacks that move slab data between ranks (multi-GPU slab
 // partition; implemented over torch.distributed / NCCL by the host layer).
 // All are stream-ordered on the stream they are given.
+// Level codes of the exchanges: 0, 1 = slab levels in the node layout (doubles
+// or floats per node plane 3 (nx+1)(ny+1)); kP32Level = level 0 in the P32
+// layout (3 * XS * (ny+1) floats per node plane, sg_fine_pk.cu).
+constexpr int kP32Level = 2;
 struct CommHooks {
   void* ctx = nullptr;
   // fill the ghost node planes of a window vector of distributed level `level`
@@ -67,6 +73,7 @@ struct Level {
   int64_t n32() const { return p32_size(g->d); }
 };
 
+struct DistPart;
 struct Hier {
   FineOp* fine = nullptr;
   std::vector<std::unique_ptr<Level>> lv;
@@ -84,6 +91,8 @@ struct Hier {
   cudaGraphExec_t graph[3] = {nullptr, nullptr, nullptr};
   size_t graph_nodes[3] = {0, 0, 0};
   const CommHooks* comm = nullptr;  // slab windows: halo before every level apply
+  DistPart* dist = nullptr;         // slab windows: the part (coarse-tail transition)
+  bool released = false;  // slab levels freed for a slab solve (dist_release_full)
   ~Hier();
 };
 // One V/W-cycle from lv[0]->w.r into lv[0]->w.x, replayed from a CUDA graph
@@ -160,6 +169,17 @@ struct NativeSys {
 };
 
 // ------------------------------------------------------ multi-GPU slabs
+// Device-side transport (sg_peer.cu): halo / rank-ordered sum / allgather as
+// kernels storing into the peer ranks' IPC-mapped mailboxes.
+struct PeerComm;
+std::vector<std::array<int, 4>> halo_pieces(const std::vector<std::array<int, 4>>& win);
+PeerComm* peer_create(int rank, int world, int n_dist, const int* planes_all, const int64_t* pnd,
+                      const int* full_planes, int64_t p32_plane, cudaStream_t s, CommHooks& hooks);
+void peer_destroy(PeerComm* p);
+void peer_handle(PeerComm* p, void* out);
+unsigned long long peer_base(PeerComm* p);
+void peer_open(PeerComm* p, const void* handles, const unsigned long long* ptrs);
+
 // One rank's part of a slab-partitioned hierarchy: levels 0..n_dist-1 are
 // z-slab windows (owned node planes + ghost planes), the coarser levels are
 // the replicated full hierarchy `full` (visited after an allgather of the
@@ -173,6 +193,12 @@ struct DistPart {
   FineWork wfw;                  // its solver scratch
   std::unique_ptr<Hier> W;       // window levels (W->lv[0] fine window, W->lv[1] L1 window)
   DBuf<double> bfull, xfull;     // full level-0 node vectors (API boundary)
+  PeerComm* peer = nullptr;      // device transport (comm hooks point into it), or host hooks
+  bool full_released = false;    // replicated slab levels of `full` freed (dist_release_full)
+  // CUDA graphs of the distributed cycle (device transport only), per gamma
+  cudaGraphExec_t graph[3] = {nullptr, nullptr, nullptr};
+  size_t graph_nodes[3] = {0, 0, 0};
+  ~DistPart();
   int64_t plane_nd(int l) const { return 3 * int64_t(W->lv[size_t(l)]->g->d.nx + 1) * (W->lv[size_t(l)]->g->d.ny + 1); }
   int64_t own_off(int l) const { return (o0[l] - w0[l]) * plane_nd(l); }
   int64_t own_n(int l) const { return (o1[l] - o0[l]) * plane_nd(l); }
@@ -181,6 +207,11 @@ std::unique_ptr<DistPart> dist_build(Hier& full, int n_dist, const int* planes, 
                                      cudaStream_t s);
 // one distributed V/W-cycle: W->lv[0]->w.r -> W->lv[0]->w.x
 void dist_cycle(DistPart& D, int gamma, cudaStream_t s);
+// the same, replayed from a CUDA graph when the transport is device-side
+void dist_cycle_run(DistPart& D, int gamma, cudaStream_t s);
+// free the replicated full-grid copies of the slab levels (stencils, work
+// vectors) that the windows replaced; the coarse tail keeps what it reads
+void dist_release_full(DistPart& D, cudaStream_t s);
 
 void pcg_native(NativeSys& sys, const double* b_node, double* x_node, const SolverCfg& cfg,
                 SolveOut& out, std::vector<double>& hist, cudaStream_t s);

@@ -319,7 +319,7 @@ struct Ctx {
     if (sys.hier) {
       Level& L0 = *sys.hier->lv[0];
       if (r != L0.w.r.p) copy_k<<<nb256(nd), 256, 0, s>>>(nd, r, L0.w.r.p);
-      if (sys.dist) dist_cycle(*sys.dist, sys.gamma, s);
+      if (sys.dist) dist_cycle_run(*sys.dist, sys.gamma, s);
       else cycle_run(*sys.hier, sys.gamma, s);
       if (z != L0.w.x.p) copy_k<<<nb256(nd), 256, 0, s>>>(nd, L0.w.x.p, z);
     } else {

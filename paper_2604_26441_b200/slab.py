@@ -18,10 +18,17 @@ the deeper levels gathered.  This module is that layer:
   ordered sum of a few doubles, allgather of owned planes) on torch tensors
   over ``torch.distributed``: NCCL on CUDA tensors, or gloo (host staged).
 * ``SlabSolver`` -- one rank's handle: builds its windows in libsg_b200.so
-  (``sg_dist_create``) from the replicated hierarchy and runs the native
-  PCG / FGMRES drivers over them (``sg_dist_solve``), the library calling back
-  into ``TorchSlabComm`` for each exchange.  Every rank passes the same global
-  ``b`` and receives the same global ``x``.
+  from the replicated hierarchy and runs the native PCG / FGMRES drivers over
+  them (``sg_dist_solve``).  Two transports:
+    - ``"peer"`` (default with NCCL): the exchanges are device kernels that
+      store into the other ranks' mailboxes (CUDA IPC mappings over NVLink,
+      ``sg_dist_create_peer``, csrc/sg_peer.cu) and signal with system-scope
+      flags -- no host step inside a solve iteration except the one scalar
+      read of the PCG driver, and the distributed cycle replays from a CUDA
+      graph.
+    - ``"torch"``: the library calls back into ``TorchSlabComm`` for each
+      exchange (gloo / NCCL through torch.distributed).
+  Every rank passes the same global ``b`` and receives the same global ``x``.
 
 Levels below the slab levels are replicated on every rank: the cut level's
 residual is allgathered, each rank runs the coarse tail, and slices its own
@@ -118,6 +125,17 @@ def halo_pieces(plan_level):
     return out
 
 
+#: exchange level of level-0 vectors in the P32 layout (csrc/sg_hier.cuh kP32Level)
+P32_LEVEL = 2
+
+
+def p32_xs(nx: int) -> int:
+    """Row stride of the P32 layout (csrc/sg_fine_pk.cu p32_xs): NX = nx + 1
+    rounded up to a multiple of 32 up to 256, else to even."""
+    nx1 = nx + 1
+    return (nx1 + 31) & ~31 if nx1 <= 256 else (nx1 + 1) & ~1
+
+
 class TorchSlabComm:
     """Slab data movement on torch tensors over a torch.distributed group.
 
@@ -138,7 +156,7 @@ class TorchSlabComm:
         self.full_planes = list(full_planes)
         self.backend = dist.get_backend(group)
         self.nccl = self.backend == "nccl"
-        self.pieces = [halo_pieces(lv) for lv in plan]
+        self.pieces = [halo_pieces(lv) if lv is not None else [] for lv in plan]
         self.n_halo = 0
         self.n_gather = 0
         self.n_sum = 0
@@ -248,16 +266,41 @@ def _guarded(fn):
     return call
 
 
+class _TorchRank:
+    def __init__(self, group):
+        import torch.distributed as dist
+        self.dist, self.group = dist, group
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+
+    def barrier(self):
+        self.dist.barrier(self.group)
+
+    def all_gather_object(self, obj):
+        out = [None] * self.world
+        self.dist.all_gather_object(out, obj, group=self.group)
+        return out
+
+
 class SlabSolver:
     """This rank's part of a slab-partitioned solve of ``op`` preconditioned by
     ``hierarchy`` (built identically on every rank).
 
     ``n_dist`` slab levels (default: 2 when the hierarchy has >= 3 levels and
     even nz, else 1); the rest of the hierarchy is the replicated coarse tail.
+    ``transport``: "peer" (device kernels over IPC-mapped mailboxes), "torch"
+    (host callbacks into TorchSlabComm) or "auto" (peer with NCCL, torch
+    otherwise).  ``group``: a torch.distributed group (None = WORLD).  One
+    process per GPU: a peer wait kernel spins on the device, so ranks sharing
+    a CUDA context (threads) could deadlock on an implicitly synchronising
+    runtime call (cudaFree) in another rank.
+    ``release_full``: free the hierarchy's replicated full-grid copies of the
+    slab levels once the windows exist (the hierarchy's own single-GPU cycle
+    is then unavailable); only the windows and the coarse tail stay resident.
     """
 
-    def __init__(self, op, hierarchy, group=None, n_dist=None):
-        import torch.distributed as dist
+    def __init__(self, op, hierarchy, group=None, n_dist=None, transport="auto",
+                 release_full=False):
         from . import _dev
         if hierarchy._op is not op:
             raise ValueError("hierarchy built for a different operator")
@@ -269,18 +312,37 @@ class SlabSolver:
             n_dist = 2 if (nl >= 3 and g.nz % 2 == 0) else 1
         if n_dist >= nl:
             raise ValueError("need a replicated level below the slab levels")
-        world = dist.get_world_size(group)
+        grp = _TorchRank(group)
+        world, rank = grp.world, grp.rank
+        if transport == "auto":
+            transport = "peer" if grp.dist.get_backend(group) == "nccl" else "torch"
+        if transport not in ("peer", "torch"):
+            raise ValueError(f"unknown slab transport {transport!r}")
+        self.transport = transport
+        self._grp = grp
         self.plan = slab_plan(g.nz, world, n_dist)
         dims = [hierarchy.levels[l]._dims for l in range(n_dist)]
         psz = [3 * (nx + 1) * (ny + 1) for nx, ny, _ in dims]
         fpl = [nz + 1 for _, _, nz in dims]
-        self.comm = TorchSlabComm(self.plan, psz, fpl, group)
+        # exchange level 2 (P32_LEVEL): level 0 in the P32 layout of the FP32
+        # level-0 smoother -- the same planes, 3 * XS * (ny + 1) floats each
+        while len(psz) < P32_LEVEL:
+            psz.append(0)
+            fpl.append(0)
+        psz.append(3 * p32_xs(g.nx) * (g.ny + 1))
+        fpl.append(g.nz + 1)
+        plan_x = list(self.plan) + [None] * (P32_LEVEL - n_dist) + [self.plan[0]]
+        self.comm = TorchSlabComm(plan_x, psz, fpl, group) if transport == "torch" else None
         self.op, self.hierarchy, self.n_dist = op, hierarchy, n_dist
         self._psz = psz
-        rank = self.comm.rank
         mine = [self.plan[l][rank] for l in range(n_dist)]
-        self._nwin = [w.n_planes * p for w, p in zip(mine, psz)]
+        mine_x = mine + [None] * (P32_LEVEL - n_dist) + [mine[0]]
+        self._nwin = [w.n_planes * p if w else 0 for w, p in zip(mine_x, psz)]
         self._nfull = [f * p for f, p in zip(fpl, psz)]
+        self._lib = _native.load()
+        if transport == "peer":
+            self._init_peer(hierarchy, n_dist, rank, world, release_full)
+            return
         c = self.comm
 
         def halo(_ctx, level, vec, eb, _stream):
@@ -297,17 +359,42 @@ class SlabSolver:
                                 _native.ALLREDUCE_FN(_guarded(allreduce)),
                                 _native.ALLGATHER_FN(_guarded(allgather)))
         planes = np.array([[w.w0, w.w1, w.o0, w.o1] for w in mine], dtype=np.int32)
-        self._lib = _native.load()
         h = ctypes.c_void_p()
-        dist.barrier(group)  # first collective of the group before any P2P
+        grp.barrier()  # first collective of the group before any P2P
         _native.check(self._lib.sg_dist_create(hierarchy._hh, n_dist, planes.ctypes.data,
                                                ctypes.byref(self._cbs), _dev.stream(),
                                                ctypes.byref(h)))
         self._hd = h
+        if release_full:
+            _native.check(self._lib.sg_dist_release_full(self._hd, _dev.stream()))
+
+    def _init_peer(self, hierarchy, n_dist, rank, world, release_full):
+        """Device transport: create the mailbox, exchange its CUDA IPC handle
+        over the process group and map every peer's."""
+        from . import _dev
+        planes = np.array([[[w.w0, w.w1, w.o0, w.o1] for w in (self.plan[l][r] for l in range(n_dist))]
+                           for r in range(world)], dtype=np.int32)
+        h = ctypes.c_void_p()
+        _native.check(self._lib.sg_dist_create_peer(hierarchy._hh, n_dist, planes.ctypes.data, rank,
+                                                    world, _dev.stream(), ctypes.byref(h)))
+        self._hd = h
+        handle = (ctypes.c_char * 64)()
+        base = ctypes.c_uint64()
+        _native.check(self._lib.sg_dist_peer_handle(h, handle, ctypes.byref(base)))
+        hs = self._grp.all_gather_object(bytes(handle))
+        _native.check(self._lib.sg_dist_peer_open(h, b"".join(hs), None))
+        if release_full:
+            _native.check(self._lib.sg_dist_release_full(h, _dev.stream()))
+        self._grp.barrier()  # every mailbox mapped and zeroed before the first exchange
 
     def close(self):
         hd = getattr(self, "_hd", None)
         if hd is not None and hd.value:
+            if getattr(self, "transport", "torch") == "peer":
+                # no rank unmaps / frees its mailbox while another may still store into it
+                import torch
+                torch.cuda.current_stream().synchronize()
+                self._grp.barrier()
             self._lib.sg_dist_destroy(hd)
             self._hd = None
 
@@ -367,9 +454,9 @@ class SlabSolver:
         return self.solve(b, cfg, "fgmres")
 
 
-def slab_pcg(op, hierarchy, b, cfg, group=None):
+def slab_pcg(op, hierarchy, b, cfg, group=None, transport="auto"):
     """One-shot slab-partitioned ``pcg(op.matvec, hierarchy.vcycle, b, cfg)``."""
-    s = SlabSolver(op, hierarchy, group)
+    s = SlabSolver(op, hierarchy, group, transport=transport)
     try:
         return s.pcg(b, cfg)
     finally:

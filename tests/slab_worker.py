@@ -72,7 +72,7 @@ def _solve_case(out):
         cfg = P.SolverConfig(tol=1e-6, maxiter=200)
         key = f"{nx}x{ny}x{nz}_{kind}_{policy}"
         for n_dist in (1, 2):
-            s = SlabSolver(op, h, n_dist=n_dist)
+            s = SlabSolver(op, h, n_dist=n_dist, transport=os.environ.get("SLAB_TRANSPORT", "torch"))
             kx = s.matvec(x)
             vx = s.vcycle(x)
             rep = s.pcg(b, cfg)
@@ -91,7 +91,10 @@ def _solve_case(out):
                                       zip(rep.residual_history, rep1.residual_history))),
                 "x_rel": float(np.abs(rep.x - rep1.x).max() / np.abs(rep1.x).max()),
                 "true_res": rep.final_true_residual,
-                "halos": s.comm.n_halo, "gathers": s.comm.n_gather, "sums": s.comm.n_sum,
+                "halos": s.comm.n_halo if s.comm else -1,
+                "gathers": s.comm.n_gather if s.comm else -1,
+                "sums": s.comm.n_sum if s.comm else -1,
+                "transport": s.transport,
             }
             if n_dist == 2 and policy == "fp32":
                 rf = s.fgmres(b, P.SolverConfig(method="fgmres", tol=1e-6, maxiter=200, restart=32))
@@ -101,6 +104,19 @@ def _solve_case(out):
                                                 "fg_iters1": rf1.iterations,
                                                 "fg_conv": rf.converged})
             s.close()
+        # release_full: the hierarchy's replicated slab levels freed; the slab
+        # solve must not depend on them (same x as the solve above, bit for bit)
+        s = SlabSolver(op, h, n_dist=2, transport=os.environ.get("SLAB_TRANSPORT", "torch"),
+                       release_full=True)
+        rep_r = s.pcg(b, cfg)
+        res[f"{key}_released"] = {"x_equal": bool(np.array_equal(rep_r.x, rep.x)),
+                                  "iters": rep_r.iterations}
+        try:
+            h.vcycle(x)
+            res[f"{key}_released"]["vcycle_raises"] = False
+        except Exception:
+            res[f"{key}_released"]["vcycle_raises"] = True
+        s.close()
     return res
 
 

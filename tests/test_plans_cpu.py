@@ -84,3 +84,27 @@ def test_p32_tiling_owns_every_node_once(dims):
     for c in range(pl["nch"]):
         zown[c * pl["kchunk"]:min((c + 1) * pl["kchunk"], nz + 1)] += 1
     assert (zown == 1).all()
+
+
+def test_native_halo_pieces_match_python():
+    """sg_plan_halo (the device transport's transfer lists, csrc/sg_peer.cu) and
+    slab.py halo_pieces (the torch transport's) enumerate the same ghost pieces."""
+    import ctypes
+    import numpy as np
+    from paper_2604_26441_b200 import _native
+    from paper_2604_26441_b200.slab import halo_pieces, slab_plan
+    lib = _native.load()
+    for nz in (4, 6, 8, 12, 20, 50, 100):
+        for world in range(1, 9):
+            for n_dist in (1, 2):
+                try:
+                    plan = slab_plan(nz, world, n_dist)
+                except ValueError:
+                    continue
+                for lv in plan:
+                    w = np.array([[x.w0, x.w1, x.o0, x.o1] for x in lv], dtype=np.int32)
+                    out = np.zeros(4 * 64 + 1, dtype=np.int32)
+                    assert lib.sg_plan_halo(world, w.ctypes.data, out.ctypes.data, 64) == 0
+                    n = int(np.argmax(out == -1)) // 4
+                    got = [tuple(int(v) for v in out[4 * i:4 * i + 4]) for i in range(n)]
+                    assert got == [tuple(p) for p in halo_pieces(lv)], (nz, world, n_dist)

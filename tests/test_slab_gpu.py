@@ -14,16 +14,23 @@ from test_slab_cpu import run_ranks
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("world", [1, 2, 3])
-def test_slab_solver_matches_single_gpu(world, tmp_path, monkeypatch):
+@pytest.mark.parametrize("world,transport", [(1, "torch"), (2, "torch"), (3, "torch"),
+                                             (1, "peer"), (2, "peer"), (3, "peer")])
+def test_slab_solver_matches_single_gpu(world, transport, tmp_path, monkeypatch):
     # slab windows run the full stencil; so does the single-GPU comparison here
-    # (its default is the symmetric copy, ~1e-16 apart: test_symmetric_stencil_*)
+    # (its default is the symmetric copy, ~1e-16 apart: test_symmetric_stencil_*).
+    # transport "peer": device kernels over CUDA IPC mailboxes (csrc/sg_peer.cu);
+    # the ranks are processes sharing the one GPU of this box.
     monkeypatch.setenv("SG_ST64_FULL", "1")
+    monkeypatch.setenv("SLAB_TRANSPORT", transport)
     res = run_ranks("solve", world, tmp_path / "solve.json", timeout=900)
     assert len(res) == world
     for r in res:
         assert r == res[0]  # every rank returns the same global results
     for key, v in res[0].items():
+        if key.endswith("_released"):
+            assert v["x_equal"] and v["vcycle_raises"], (key, v)
+            continue
         assert v["matvec_equal"], (key, v)
         assert v["vcycle_equal"], (key, v)
         assert v["conv"] == v["conv1"], (key, v)
@@ -31,9 +38,27 @@ def test_slab_solver_matches_single_gpu(world, tmp_path, monkeypatch):
             assert v["hist_equal"] and v["iters"] == v["iters1"], (key, v)
         else:
             assert abs(v["iters"] - v["iters1"]) <= 2, (key, v)
-            assert v["halos"] > 0 and v["gathers"] > 0 and v["sums"] > 0
+            assert v["transport"] == transport
+            if transport == "torch":
+                assert v["halos"] > 0 and v["gathers"] > 0 and v["sums"] > 0
         if v["conv"]:
             assert v["true_res"] < 1e-6
             assert v["x_rel"] < 1e-4, (key, v)
         if "fg_iters" in v:
             assert v["fg_conv"] and abs(v["fg_iters"] - v["fg_iters1"]) <= 2, (key, v)
+
+
+
+@pytest.mark.gpu
+def test_slab_peer_symmetric_stencil(tmp_path, monkeypatch):
+    """Windows on the symmetric level-1 copy (the single-GPU default): owned rows
+    read their lower blocks from ghost-plane neighbours, bit-identical to one GPU."""
+    monkeypatch.delenv("SG_ST64_FULL", raising=False)
+    monkeypatch.setenv("SLAB_TRANSPORT", "peer")
+    res = run_ranks("solve", 2, tmp_path / "solve.json", timeout=900)
+    for key, v in res[0].items():
+        if key.endswith("_released"):
+            assert v["x_equal"] and v["vcycle_raises"], (key, v)
+            continue
+        assert v["matvec_equal"] and v["vcycle_equal"], (key, v)
+        assert abs(v["iters"] - v["iters1"]) <= 2, (key, v)
