@@ -134,15 +134,18 @@ void fine_apply_f32(const FineOp& op, const float* u, float* y, cudaStream_t s) 
 void fine_apply_bf16_dense(const FineOp& op, const float* u, float* y, cudaStream_t s) {
   launch_apply<float, 2>(op.grid.d, op.grid.nmask.p, u, y, op.E32.p, op.ke16, s);
 }
-// BF16EMU runs on the tensor cores (tcgen05, sg_fine_tc.cu); SG_BF16_DENSE=1
-// selects the CUDA-core reference kernel (used by the parity tests).
+// BF16EMU runs on the tensor cores: the record-fed pipelined kernel
+// (sg_fine_tc2.cu), or for grids wider than it supports the per-element one
+// (sg_fine_tc.cu, also SG_BF16_TC1=1); SG_BF16_DENSE=1 selects the CUDA-core
+// reference kernel (used by the parity tests).
 void fine_apply_bf16(const FineOp& op, const float* u, float* y, cudaStream_t s) {
   static const bool dense = [] {
     const char* e = std::getenv("SG_BF16_DENSE");
     return e && e[0] == '1';
   }();
+  static const bool tc1 = std::getenv("SG_BF16_TC1") != nullptr;  // per-element staging kernel
   if (dense) fine_apply_bf16_dense(op, u, y, s);
-  else fine_apply_bf16_tc(op, u, y, s);
+  else if (tc1 || !fine_apply_bf16_tc2(op, u, y, s)) fine_apply_bf16_tc(op, u, y, s);
 }
 
 void fine_diag_raw(const FineOp& op, double* d, cudaStream_t s) {

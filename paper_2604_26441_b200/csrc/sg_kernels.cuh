@@ -77,6 +77,7 @@ void stencil_res64(const Grid& g, const double* At, const double* x, const doubl
                    cudaStream_t s);
 int kKwColHost(int q);
 bool p64_supported(const FineOp& op);
+bool fine_apply_bf16_tc2(const FineOp& op, const float* u, float* y, cudaStream_t s);
 void fine_apply_p64(const FineOp& op, const double* u, double* y, cudaStream_t s);
 void make_state_device(int kind, int nx, int ny, int nz, double vf, double floor_,
                        unsigned long long seed, double* rho, cudaStream_t s);

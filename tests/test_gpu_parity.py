@@ -304,6 +304,33 @@ def test_fine_apply_fp64_block_tiling(dims, kind):
     assert np.array_equal(y, op.matvec_tagged(u, P.PrecisionTag.FP64))
 
 
+@pytest.mark.parametrize("dims,kind", [((100, 100, 100), "uniform"), ((131, 7, 5), "binary"),
+                                       ((9, 33, 17), "random_floor"), ((1, 1, 1), "uniform"),
+                                       ((2, 61, 3), "binary"), ((200, 3, 2), "binary"),
+                                       ((600, 2, 2), "random_floor"), ((63, 40, 9), "binary")])
+def test_fine_apply_bf16_tiling(dims, kind):
+    """BF16EMU apply on the record-fed tcgen05 kernel (sg_fine_tc2.cu) across tile
+    shapes -- rows chained through the phantom column, partial last tiles, one
+    element -- and the per-element kernel it falls back to for NX > 512 (600 x 2 x 2)."""
+    g, op, og, E, ke = _pair(dims, kind)
+    u32 = P.SplitMix64(6).gaussian(g.n_free).astype(np.float32)
+    y = op.matvec_tagged(u32, P.PrecisionTag.BF16EMU)
+    assert _rel(y, O.fine_apply(og, E, ke, u32, "bf16")) < 1e-6
+    assert np.array_equal(y, op.matvec_tagged(u32, P.PrecisionTag.BF16EMU))
+
+
+def test_fine_apply_bf16_general_mask():
+    nx, ny, nz = 14, 9, 6
+    rng = np.random.default_rng(5)
+    mask = rng.random(3 * (nx + 1) * (ny + 1) * (nz + 1)) < 0.2
+    g = P.make_grid(nx, ny, nz, mask)
+    op = P.FineOperator(g, P.simp_modulus(P.make_state("binary", nx, ny, nz, vf=0.5, seed=42), 3.0))
+    og = O.make_grid(nx, ny, nz, mask)
+    u32 = P.SplitMix64(10).gaussian(g.n_free).astype(np.float32)
+    assert _rel(op.matvec_tagged(u32, P.PrecisionTag.BF16EMU),
+                O.fine_apply(og, op.modulus.E, op.ke, u32, "bf16")) < 1e-6
+
+
 def test_fine_apply_fp64_general_mask():
     nx, ny, nz = 14, 9, 6
     rng = np.random.default_rng(4)
