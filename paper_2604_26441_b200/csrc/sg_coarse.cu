@@ -302,6 +302,8 @@ struct BrickArgs {
   int sx, sy, sz;
   int nrep;            // variant 3: replicas of the partial-packet array (spread L2 polling)
   int poll_ns;         // variant 3: back-off between polling passes
+  int recip;           // variant 2: beta, beta*gamma/alpha_prev from reciprocals formed
+                       // during the halo wait (one division on the critical path, not three)
   long long* trace;
 };
 
@@ -1245,6 +1247,7 @@ __global__ void __launch_bounds__(br_threads(kVar), 1) pcg80_brick_kernel(BrickA
     }
     unsigned epoch = 0;
     double gprev = 0.0, aprev = 0.0;
+    double igprev = 0.0, iaprev = 0.0;  // 1/gamma_prev, 1/alpha_prev (formed off the critical path)
     for (int s = 0; s < P.steps; ++s) {
       stamp_s(P.trace, s, 0);
       // m = D^-1 w to the neighbours; (r.u, w.u) published
@@ -1257,6 +1260,10 @@ __global__ void __launch_bounds__(br_threads(kVar), 1) pcg80_brick_kernel(BrickA
       ++epoch;
       br_publish2(lg, ld, P, fbase | epoch, red);
       stamp_s(P.trace, s, 1);
+      if (P.recip && s > 0) {  // the halo polls below wait anyway
+        igprev = 1.0 / gprev;
+        iaprev = 1.0 / aprev;
+      }
       fill_ph(unsigned(s) + 1u);
       __syncthreads();
       stamp_s(P.trace, s, 5);
@@ -1333,8 +1340,13 @@ __global__ void __launch_bounds__(br_threads(kVar), 1) pcg80_brick_kernel(BrickA
       double beta = 0.0, pap = del;
       if (s > 0) {
         if (!(gam > 0.0) || !isfinite(gam)) break;
-        beta = gam / gprev;
-        pap = del - beta * gam / aprev;
+        if (P.recip) {
+          beta = gam * igprev;
+          pap = del - (beta * gam) * iaprev;
+        } else {
+          beta = gam / gprev;
+          pap = del - beta * gam / aprev;
+        }
       }
       if (!(pap > 0.0) || !isfinite(pap)) break;
       const double al = gam / pap;
@@ -1646,6 +1658,11 @@ void Pcg80::solve(const double* b, double* x, cudaStream_t s) {
     a.sz = sz;
     a.nrep = nrep;
     a.poll_ns = poll_ns;
+    static const int recip = [] {  // SG_PCG80_RECIP=0: the three divisions (A/B)
+      const char* e = std::getenv("SG_PCG80_RECIP");
+      return e && e[0] == '0' ? 0 : 1;
+    }();
+    a.recip = recip;
     a.trace = trace;
     void* args[] = {&a};
     void* fn = variant == 3 ? (void*)pcg80_brick_kernel<3>
