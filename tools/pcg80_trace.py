@@ -13,9 +13,9 @@ with warnings.catch_warnings():
     h = P.build_hierarchy(op, 4, "fp32")
 h.vcycle(np.ones(g.n_free))
 for rep in range(3):
-    t = np.zeros(8 * 256, dtype=np.int64)
+    t = np.zeros(64 * 256, dtype=np.int64)  # sg_hier_pcg80_trace writes 8 steps x 8 stamps per block
     _native.check(lib.sg_hier_pcg80_trace(h._hh, t.ctypes.data, _dev.stream()))
-    t = t.reshape(256, 8)
+    t = t.reshape(256, 8, 8)[:, 0, :]  # step 8 of every block
     t = t[t[:, 0] > 0]
     t0 = t[:, 0].min()
     rel = (t - t0) / 1e3
