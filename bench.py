@@ -268,7 +268,14 @@ def run_gpu(args):
         # slab partition of levels 0-1 over the ranks (NCCL halos / dot sums),
         # coarse tail replicated (paper_2604_26441_b200/slab.py)
         from paper_2604_26441_b200.slab import SlabSolver
-        slab = SlabSolver(op, h, transport=args.transport, release_full=True)
+        try:
+            slab = SlabSolver(op, h, transport=args.transport, release_full=True)
+        except Exception as exc:  # e.g. no CUDA IPC between these devices: host transport
+            if args.transport != "peer":
+                raise
+            print(f"peer transport unavailable ({exc!r}); using torch.distributed", file=sys.stderr)
+            args.transport = "torch"
+            slab = SlabSolver(op, h, transport="torch", release_full=True)
         solve = lambda b: slab.pcg(b, cfg)
     else:
         solve = lambda b: P.pcg(op.matvec, h.vcycle, b, cfg)
@@ -360,11 +367,14 @@ def run_gpu(args):
                                 "(pageable H2D/D2H inside P.pcg)"}
 
     achieved = b32 / (t32 * 1e-3) / 1e9
-    traffic = None
+    # DRAM bytes of one launch from the committed ncu capture (ncu cannot run
+    # inside the timed process); its provenance travels with the number
+    traffic, traffic_src = None, None
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tpath):
         try:
-            traffic = json.load(open(tpath)).get("fine_apply_fp32_bytes")
+            tj = json.load(open(tpath))
+            traffic, traffic_src = tj.get("fine_apply_fp32_bytes"), tj.get("source")
         except Exception:
             traffic = None
     line = {
@@ -378,7 +388,7 @@ def run_gpu(args):
         "fine_matvec_gbs": achieved,
         "roofline": {"kernel": "fine_apply_fp32 (fine_pk_kernel<0>, packed FP32x2, P32 layout)", "bound": "hbm",
                      "achieved": achieved, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": traffic,
+                     "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
                      "alg_bytes_per_launch": b32, "launch_ms": t32},
         "components": comps,
         "e2e": {"value": e2e_s, "unit": "s", "h2d_bytes_per_step": 8 * n_free,
