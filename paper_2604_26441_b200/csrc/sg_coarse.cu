@@ -277,6 +277,11 @@ constexpr int kBrLn = kBrCap + (kBrBlock - kBrThreads);  // row pitch of the per
 constexpr int kBrRegRows = 3;                // q9 = 0..2 (dj = -1) kept in registers
 constexpr int kBrSmRows = 9 - kBrRegRows;
 constexpr int kBrWinMax = 448;               // halo-window nodes
+// pipelined variant: window rows stored at stride bx + 16 (row r of a warp's
+// lanes then starts at bank residue r*bx mod 16, as if the rows were packed:
+// the 64-bit window reads of a half-warp hit 16 distinct bank pairs), per
+// component kBrWinS doubles; other variants / oversized windows: stride bx + 2
+constexpr int kBrWinS = 1024;
 constexpr int kBrFill = (3 * kBrWinMax + kBrBlock - 1) / kBrBlock;
 constexpr int kBrOwnVec = 9 * kBrLn;        // pipelined variant: [part][comp][kBrLn] SpMV partials
 constexpr int kBrStage = 2 * 160;            // pipelined variant: staged partial packets
@@ -302,6 +307,7 @@ struct BrickArgs {
   int sx, sy, sz;
   int nrep;            // variant 3: replicas of the partial-packet array (spread L2 polling)
   int poll_ns;         // variant 3: back-off between polling passes
+  int winpad;          // variant 2: padded window rows (conflict-free half-warp reads)
   int recip;           // variant 2: beta, beta*gamma/alpha_prev from reciprocals formed
                        // during the halo wait (one division on the critical path, not three)
   long long* trace;
@@ -555,8 +561,9 @@ __device__ __forceinline__ void tm_ld18(uint32_t addr, double (&v)[9]) {
 __host__ __device__ constexpr int br_smem_a(int var) {
   return 3 * (9 - (var >= 2 ? kBrTmRows : kBrRegRows)) * 9 * kBrCap;
 }
+__host__ __device__ constexpr int br_win_cs(int var) { return var == 2 ? kBrWinS : kBrWinMax; }
 __host__ __device__ constexpr int br_smem_bytes(int var) {
-  return int(sizeof(double)) * (br_smem_a(var) + 3 * kBrWinMax + kBrOwnVec) +
+  return int(sizeof(double)) * (br_smem_a(var) + 3 * br_win_cs(var) + kBrOwnVec) +
          int(sizeof(uint4)) * kBrStage +
          (var == 3 ? int(sizeof(double)) * (3 * kBrWinMax + 3 * kBrFill * kBrBlock) : 0);
 }
@@ -613,8 +620,9 @@ __global__ void __launch_bounds__(br_threads(kVar), 1) pcg80_brick_kernel(BrickA
   // register (TMEM for the pipelined variants) rows / shared-memory rows
   constexpr int kRR = kVar >= 2 ? kBrTmRows : kBrRegRows, kSR = 9 - kRR;
   double* smA = smdyn;             // [(part*kSR + row)*9 + entry][kBrCap]
-  double* pw = smdyn + br_smem_a(kVar);  // [3][kBrWinMax] p on the brick + halo
-  double* ov = pw + 3 * kBrWinMax;  // [3][3][kBrLn] SpMV partials (pipelined variant)
+  double* pw = smdyn + br_smem_a(kVar);  // [3][CS] p on the brick + halo
+  constexpr int CS = br_win_cs(kVar);  // window doubles per component
+  double* ov = pw + 3 * CS;  // [3][3][kBrLn] SpMV partials (pipelined variant)
   uint4* pst = reinterpret_cast<uint4*>(ov + kBrOwnVec);  // [2][160] staged packets
   __shared__ double rowpart[2][3][kBrLn];
   __shared__ double red[32];
@@ -629,6 +637,7 @@ __global__ void __launch_bounds__(br_threads(kVar), 1) pcg80_brick_kernel(BrickA
             bz = (bzi + 1) * NZ / P.sz - z0;
   const int nloc = bx * by * bz;
   const int WX = bx + 2, WY = by + 2, WZ = bz + 2, wn = WX * WY * WZ;
+  const int WXS = (kVar == 2 && P.winpad && (bx + 16) * WY * WZ <= CS) ? bx + 16 : WX;  // storage row stride
   const int t = threadIdx.x;
   // threads past 3*kBrCap (warp padding) are part 2 with ln >= kBrCap: never active
   const int part = min(t / kBrCap, 2), ln = t - part * kBrCap;
@@ -739,14 +748,14 @@ __global__ void __launch_bounds__(br_threads(kVar), 1) pcg80_brick_kernel(BrickA
       const int c = iw / wn, w = iw - c * wn;
       const int wx = w % WX, wy = (w / WX) % WY, wz = w / (WX * WY);
       const int gx = x0 - 1 + wx, gy = y0 - 1 + wy, gz = z0 - 1 + wz;
-      fw[k] = c * kBrWinMax + w;
+      fw[k] = c * CS + (wz * WY + wy) * WXS + wx;
       if (gx >= 0 && gx < NX && gy >= 0 && gy < NY && gz >= 0 && gz < NZ)
         fg[k] = c * nn + gx + NX * (gy + NY * gz);
     }
   }
 
-  const int wbase = ((lz + part) * WY + ly) * WX + lx;
-  const int wctr = ((lz + 1) * WY + ly + 1) * WX + lx + 1;
+  const int wbase = ((lz + part) * WY + ly) * WXS + lx;
+  const int wctr = ((lz + 1) * WY + ly + 1) * WXS + lx + 1;
   // stage the halo window of the LL vector written with flag zf; out-of-grid
   // cells are 0.  kAxpy: pw = beta*pw + v (p window), else pw = v.
   auto fill = [&](unsigned zf, bool axpy, double beta) {
@@ -780,8 +789,8 @@ __global__ void __launch_bounds__(br_threads(kVar), 1) pcg80_brick_kernel(BrickA
 #pragma unroll
     for (int q9 = 0; q9 < 9; ++q9) {
       if (q9 == 6) mid();  // hook two thirds into the stencil work
-      const int w = wbase + (q9 / 3) * WX + q9 % 3;
-      const double pv0 = pw[w], pv1 = pw[kBrWinMax + w], pv2 = pw[2 * kBrWinMax + w];
+      const int w = wbase + (q9 / 3) * WXS + q9 % 3;
+      const double pv0 = pw[w], pv1 = pw[CS + w], pv2 = pw[2 * CS + w];
       double a[9];
 #pragma unroll
       for (int e = 0; e < 9; ++e)
@@ -833,8 +842,8 @@ __global__ void __launch_bounds__(br_threads(kVar), 1) pcg80_brick_kernel(BrickA
 #pragma unroll
       for (int q9 = 0; q9 < 9; ++q9) {
         if (q9 == decltype(qmid)::value) mid();
-        const int w = wbase + (q9 / 3) * WX + q9 % 3;
-        const double pv0 = pw[w], pv1 = pw[kBrWinMax + w], pv2 = pw[2 * kBrWinMax + w];
+        const int w = wbase + (q9 / 3) * WXS + q9 % 3;
+        const double pv0 = pw[w], pv1 = pw[CS + w], pv2 = pw[2 * CS + w];
         double a[9];
         if (q9 < kRR) {
           tm_ld18(tm_row + uint32_t(q9 * 18), a);
@@ -1165,7 +1174,7 @@ __global__ void __launch_bounds__(br_threads(kVar), 1) pcg80_brick_kernel(BrickA
           stamp_s(P.trace, ts, 7);
           double lg = 0.0, ld = 0.0;
           if (act) {
-            const double mv = cur[c * kBrWinMax + wctr];
+            const double mv = cur[c * CS + wctr];
             const double n = fma(P.eps, mv, nv);
             zz = fma(beta, zz, n);
             qq = fma(beta, qq, mv);
@@ -1351,7 +1360,7 @@ __global__ void __launch_bounds__(br_threads(kVar), 1) pcg80_brick_kernel(BrickA
       if (!(pap > 0.0) || !isfinite(pap)) break;
       const double al = gam / pap;
       if (act) {
-        const double mv = pw[c * kBrWinMax + wctr];
+        const double mv = pw[c * CS + wctr];
         const double n = fma(P.eps, mv, nv);
         zz = fma(beta, zz, n);
         qq = fma(beta, qq, mv);
@@ -1402,7 +1411,7 @@ __global__ void __launch_bounds__(br_threads(kVar), 1) pcg80_brick_kernel(BrickA
       if (owner) {
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
-          zo[c] = pw[c * kBrWinMax + wctr];
+          zo[c] = pw[c * CS + wctr];
           wo[c] = fma(P.eps, zo[c], av[c]);
           lg = fma(rr[c], zo[c], lg);
           ld = fma(wo[c], zo[c], ld);
@@ -1476,7 +1485,7 @@ __global__ void __launch_bounds__(br_threads(kVar), 1) pcg80_brick_kernel(BrickA
     if (owner) {
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
-        pown[c] = pw[c * kBrWinMax + wctr];
+        pown[c] = pw[c * CS + wctr];
         qown[c] = fma(P.eps, pown[c], av[c]);
         loc = fma(pown[c], qown[c], loc);
       }
@@ -1663,6 +1672,11 @@ void Pcg80::solve(const double* b, double* x, cudaStream_t s) {
       return e && e[0] == '0' ? 0 : 1;
     }();
     a.recip = recip;
+    static const int winpad = [] {  // SG_PCG80_WINPAD=0: window rows at stride bx + 2 (A/B)
+      const char* e = std::getenv("SG_PCG80_WINPAD");
+      return e && e[0] == '0' ? 0 : 1;
+    }();
+    a.winpad = winpad;
     a.trace = trace;
     void* args[] = {&a};
     void* fn = variant == 3 ? (void*)pcg80_brick_kernel<3>
