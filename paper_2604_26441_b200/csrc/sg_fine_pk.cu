@@ -314,6 +314,7 @@ fine_pk_kernel(GridDesc g, const uint8_t* __restrict__ nmask, const float* __res
       if (own) {
         const bool left = pair > 0;
         const int64_t nodei = onode + oplane * int64_t(NX) * NY;
+        float yr[2][3];  // PK_RES: the pair's 6 values, written together below
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
           // node ex: (own e0 + left pair's e1) + (same, row above)
@@ -344,15 +345,76 @@ fine_pk_kernel(GridDesc g, const uint8_t* __restrict__ nmask, const float* __res
             *reinterpret_cast<float2*>(ep.d + o) = dn;
             const float2 xn = make_float2(__fadd_rn(xx.x, dn.x), __fadd_rn(xx.y, dn.y));
             *reinterpret_cast<float2*>(ep.xout + o) = xn;
-            if (ep.out64) {  // last smoothing step: also the f64 node-layout iterate
-              const int64_t q = 3 * nodei + c;
-              ep.out64[q] = double(xn.x);
-              if (own1) ep.out64[q + 3] = double(xn.y);
+            yr[0][c] = xn.x;  // last smoothing step: the f64 node-layout iterate (below)
+            yr[1][c] = xn.y;
+          } else {
+            yr[0][c] = y0;
+            yr[1][c] = y1;
+          }
+        }
+        if constexpr (MODE == PK_CHEB) {
+          if (ep.out64) {  // 6 contiguous doubles: 16-byte stores where aligned
+            const int64_t q = 3 * nodei;
+            double* op = ep.out64 + q;
+            if (own1) {
+              double ov[6];
+#pragma unroll
+              for (int k = 0; k < 6; ++k) ov[k] = double(yr[k / 3][k % 3]);
+              if ((q & 1) == 0) {
+#pragma unroll
+                for (int k = 0; k < 3; ++k)
+                  *reinterpret_cast<double2*>(op + 2 * k) = make_double2(ov[2 * k], ov[2 * k + 1]);
+              } else {
+                op[0] = ov[0];
+                *reinterpret_cast<double2*>(op + 1) = make_double2(ov[1], ov[2]);
+                *reinterpret_cast<double2*>(op + 3) = make_double2(ov[3], ov[4]);
+                op[5] = ov[5];
+              }
+            } else {
+#pragma unroll
+              for (int c = 0; c < 3; ++c) op[c] = double(yr[0][c]);
+            }
+          }
+        }
+        if constexpr (MODE == PK_RES) {
+          // nodes ex, ex+1 are 6 contiguous doubles in the node layout: 16-byte
+          // accesses (8 + 16 + 16 + 8 when the pair starts on an odd double)
+          // instead of six 24-byte-strided ones; same arithmetic, same bits
+          const int64_t q = 3 * nodei;
+          const double* rp = ep.r64 + q;
+          double* op = ep.out64 + q;
+          if (own1) {
+            double rv[6];
+            if ((q & 1) == 0) {
+#pragma unroll
+              for (int k = 0; k < 3; ++k) {
+                const double2 v = *reinterpret_cast<const double2*>(rp + 2 * k);
+                rv[2 * k] = v.x;
+                rv[2 * k + 1] = v.y;
+              }
+            } else {
+              rv[0] = rp[0];
+              const double2 a = *reinterpret_cast<const double2*>(rp + 1);
+              const double2 b = *reinterpret_cast<const double2*>(rp + 3);
+              rv[1] = a.x; rv[2] = a.y; rv[3] = b.x; rv[4] = b.y;
+              rv[5] = rp[5];
+            }
+            double ov[6];
+#pragma unroll
+            for (int k = 0; k < 6; ++k) ov[k] = __dsub_rn(rv[k], double(yr[k / 3][k % 3]));
+            if ((q & 1) == 0) {
+#pragma unroll
+              for (int k = 0; k < 3; ++k)
+                *reinterpret_cast<double2*>(op + 2 * k) = make_double2(ov[2 * k], ov[2 * k + 1]);
+            } else {
+              op[0] = ov[0];
+              *reinterpret_cast<double2*>(op + 1) = make_double2(ov[1], ov[2]);
+              *reinterpret_cast<double2*>(op + 3) = make_double2(ov[3], ov[4]);
+              op[5] = ov[5];
             }
           } else {
-            const int64_t q = 3 * nodei + c;
-            ep.out64[q] = __dsub_rn(ep.r64[q], double(y0));
-            if (own1) ep.out64[q + 3] = __dsub_rn(ep.r64[q + 3], double(y1));
+#pragma unroll
+            for (int c = 0; c < 3; ++c) op[c] = __dsub_rn(rp[c], double(yr[0][c]));
           }
         }
       }
