@@ -7,6 +7,7 @@
 #include <chrono>
 #include <cmath>
 #include "sg_hier.cuh"
+#include "sg_peer.cuh"
 
 namespace sg {
 
@@ -162,7 +163,7 @@ __global__ void __launch_bounds__(kRedThreads, 8) pq_step_kernel(int64_t n, doub
                                                               const double* __restrict__ p,
                                                               const double* __restrict__ q, double* sc,
                                                               double* partials, unsigned* counter,
-                                                              unsigned long long* bar) {
+                                                              unsigned long long* bar, PeerSumDev ps) {
   __shared__ double smem[8];
   __shared__ double bc;
   __shared__ bool last;
@@ -174,8 +175,16 @@ __global__ void __launch_bounds__(kRedThreads, 8) pq_step_kernel(int64_t n, doub
   if (threadIdx.x == 0) partials[blockIdx.x] = acc[0];
   const double rz = sc[S_RZ];
   grid_barrier(bar);
-  const double pq = sum_partials(partials, smem, &bc);
-  if (blockIdx.x == 0 && threadIdx.x == 0) sc[S_PQ] = pq;  // StoreTo
+  double pq = sum_partials(partials, smem, &bc);
+  if (ps.world > 1) {
+    // slab ranks: the rank-ordered sum of the local totals inside this launch
+    // (block 0 talks to the peers' mailboxes, the others wait at the barrier)
+    if (blockIdx.x == 0 && threadIdx.x == 0) sc[S_PQ] = peer_sum1(ps, pq);
+    grid_barrier(bar);
+    pq = ((volatile double*)sc)[S_PQ];
+  } else if (blockIdx.x == 0 && threadIdx.x == 0) {
+    sc[S_PQ] = pq;  // StoreTo
+  }
   // PcgStep with this step length (PcgStep::prep / load / use)
   const bool ok = isfinite(pq) && pq != 0.0 && isfinite(rz);
   const double a = ok ? __ddiv_rn(rz, pq) : 0.0;
@@ -200,30 +209,39 @@ __global__ void __launch_bounds__(kRedThreads, 8) pq_step_kernel(int64_t n, doub
   __syncthreads();
   if (!last) return;
   __threadfence();
-  const double rr = sum_partials(part2, smem, &bc);
+  double rr = sum_partials(part2, smem, &bc);
   if (threadIdx.x == 0) {  // PcgStepPost, from the values in registers
+    if (ps.world > 1) rr = peer_sum1(ps, rr);
     sc[S_OK] = ok ? 1.0 : 0.0;
     sc[S_RR] = rr;
     *counter = 0u;
   }
 }
 
-__global__ void __launch_bounds__(kRedThreads, 8) rz_pupd_kernel(int64_t n, int64_t nd,
+// (slab ranks: the dot runs over the owned range r + off, z + off (n entries),
+// the p update over the whole window (nd entries), as the unfused path)
+__global__ void __launch_bounds__(kRedThreads, 8) rz_pupd_kernel(int64_t n, int64_t nd, int64_t off,
                                                               const double* __restrict__ r,
                                                               const double* __restrict__ z,
                                                               double* __restrict__ p, double* sc,
-                                                              double* partials, unsigned long long* bar) {
+                                                              double* partials, unsigned long long* bar,
+                                                              PeerSumDev ps) {
   __shared__ double smem[8];
   __shared__ double bc;
   const int64_t stride = int64_t(gridDim.x) * kRedThreads;
   const int64_t i0 = int64_t(blockIdx.x) * kRedThreads + threadIdx.x;
   double acc[1] = {0.0};
-  for (int64_t i = i0; i < n; i += stride) acc[0] = fma(r[i], z[i], acc[0]);  // Dot
+  for (int64_t i = i0; i < n; i += stride) acc[0] = fma(r[off + i], z[off + i], acc[0]);  // Dot
   block_sum<1>(acc, smem);
   if (threadIdx.x == 0) partials[blockIdx.x] = acc[0];
   const double rz_old = sc[S_RZ];  // read by every block before block 0 replaces it
   grid_barrier(bar);
-  const double t = sum_partials(partials, smem, &bc);
+  double t = sum_partials(partials, smem, &bc);
+  if (ps.world > 1) {  // slab ranks: rank-ordered sum in this launch (see pq_step)
+    if (blockIdx.x == 0 && threadIdx.x == 0) sc[S_RZN] = peer_sum1(ps, t);
+    grid_barrier(bar);
+    t = ((volatile double*)sc)[S_RZN];
+  }
   const double beta = __ddiv_rn(t, rz_old);  // RznPost
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     sc[S_RZN] = t;
@@ -283,9 +301,13 @@ struct Ctx {
     }
   }
   // fused cooperative reduce-then-update kernels (one GPU); 0 = unavailable
+  // slab ranks on the device transport fuse the cross-rank sums into the
+  // same launches (PeerSumDev); the host transport cannot
+  PeerSumDev psum{};
+  bool psum_ok = !sys.dist || peer_sum_dev(sys.dist->peer, psum);
   int fused_blocks() {
     static int per_sm = -1;
-    if (sys.dist || std::getenv("SG_PCG_UNFUSED")) return 0;
+    if (!psum_ok || std::getenv("SG_PCG_UNFUSED")) return 0;
     if (per_sm < 0) {
       int a = 0, b = 0;
       SG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a, pq_step_kernel, kRedThreads, 0));
@@ -296,21 +318,28 @@ struct Ctx {
     return nb <= per_sm * num_sms() ? nb : 0;
   }
   void pq_step(double* x, double* r, const double* p, const double* q, int nb) {
+    // owned range only (slab ranks), as PcgStep in the unfused path
+    x += off;
+    r += off;
+    p += off;
+    q += off;
     int64_t n = nown;
     double* scp = sc.p;
     double* part = red.partials.p;
     unsigned* cnt = red.counter.p;
     unsigned long long* bar = red.gbar.p;
-    void* args[] = {&n, &x, &r, &p, &q, &scp, &part, &cnt, &bar};
+    PeerSumDev ps = psum;
+    void* args[] = {&n, &x, &r, &p, &q, &scp, &part, &cnt, &bar, &ps};
     SG_CUDA(cudaLaunchCooperativeKernel((const void*)pq_step_kernel, dim3(nb), dim3(kRedThreads), args, 0, s));
     SG_CHECK_LAUNCH();
   }
   void rz_pupd(const double* r, const double* z, double* p, int nb) {
-    int64_t n = nown, ndd = nd;
+    int64_t n = nown, ndd = nd, o = off;
     double* scp = sc.p;
     double* part = red.partials.p;
     unsigned long long* bar = red.gbar.p;
-    void* args[] = {&n, &ndd, &r, &z, &p, &scp, &part, &bar};
+    PeerSumDev ps = psum;
+    void* args[] = {&n, &ndd, &o, &r, &z, &p, &scp, &part, &bar, &ps};
     SG_CUDA(cudaLaunchCooperativeKernel((const void*)rz_pupd_kernel, dim3(nb), dim3(kRedThreads), args, 0, s));
     SG_CHECK_LAUNCH();
   }

@@ -24,37 +24,20 @@
 // rank, as TorchSlabComm.allreduce.
 #include <cstring>
 #include "sg_hier.cuh"
+#include "sg_peer.cuh"
 
 namespace sg {
 
 namespace {
 
-enum { CH_HALO = 0, CH_SUM = 1, CH_GATHER = 2 };
-constexpr int kMaxRanks = 64;
+enum { CH_HALO = PEER_CH_HALO, CH_SUM = PEER_CH_SUM, CH_GATHER = PEER_CH_GATHER };
+constexpr int kMaxRanks = kPeerMaxRanks;
 constexpr int kMaxXfer = 8;   // sends or receives of one rank on one level
-constexpr int kSumMax = 8;    // doubles per allreduce
+constexpr int kSumMax = kPeerSumMax;
 
-__device__ __forceinline__ unsigned long long ld_acq_sys(const unsigned long long* p) {
-  unsigned long long v;
-  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ void st_rel_sys(unsigned long long* p, unsigned long long v) {
-  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-// Spin until a peer's flag reaches v.  A rank that died mid-exchange must not
-// hang the device: after 60 s the kernel traps (sticky error on this rank).
-__device__ __forceinline__ void wait_geq(const unsigned long long* p, unsigned long long v) {
-  if (ld_acq_sys(p) >= v) return;
-  unsigned long long t0;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
-  while (ld_acq_sys(p) < v) {
-    __nanosleep(128);
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    if (t - t0 > 60ull * 1000000000ull) __trap();
-  }
-}
+__device__ __forceinline__ unsigned long long ld_acq_sys(const unsigned long long* p) { return peer_ld_acq(p); }
+__device__ __forceinline__ void st_rel_sys(unsigned long long* p, unsigned long long v) { peer_st_rel(p, v); }
+__device__ __forceinline__ void wait_geq(const unsigned long long* p, unsigned long long v) { peer_wait_geq(p, v); }
 
 struct Xfer {          // one contiguous plane range
   int n = 0;
@@ -464,6 +447,16 @@ void peer_handle(PeerComm* p, void* out) {
   std::memcpy(out, &h, sizeof(h));
 }
 unsigned long long peer_base(PeerComm* p) { return reinterpret_cast<unsigned long long>(p->base); }
+bool peer_sum_dev(const PeerComm* p, PeerSumDev& out) {
+  if (!p) return false;
+  for (int r = 0; r < kPeerMaxRanks; ++r) out.base[r] = r < p->world ? p->P.base[r] : nullptr;
+  out.me = p->rank;
+  out.world = p->world;
+  out.sum_off = p->off_sum;
+  out.flags_off = p->off_flags;
+  out.ep = p->ep.p;
+  return true;
+}
 void peer_open(PeerComm* p, const void* handles, const unsigned long long* ptrs) {
   p->open(static_cast<const char*>(handles), ptrs);
 }
