@@ -80,7 +80,7 @@ __device__ __forceinline__ void copy_ranges(const Xfer& X, const T* src, T* cons
 
 // halo push: my owned planes -> the receivers' slots (slot offsets in dst_off)
 template <class T>
-__global__ void halo_push_kernel(Xfer X, const T* __restrict__ vec, PeerPtrs P, int me,
+__device__ __forceinline__ void halo_push(const Xfer& X, const T* __restrict__ vec, const PeerPtrs& P, int me,
                                  size_t slot_level_off, size_t slot_bytes, int world,
                                  size_t flags_off, unsigned long long* ep, unsigned* arrive) {
   const unsigned long long e = ep[CH_HALO] + 1;
@@ -106,7 +106,7 @@ __global__ void halo_push_kernel(Xfer X, const T* __restrict__ vec, PeerPtrs P, 
 
 // halo pull: wait for every source, copy its slot into my ghost planes, ack
 template <class T>
-__global__ void halo_pull_kernel(Xfer X, T* __restrict__ vec, PeerPtrs P, int me,
+__device__ __forceinline__ void halo_pull(const Xfer& X, T* __restrict__ vec, const PeerPtrs& P, int me,
                                  size_t slot_level_off, size_t slot_bytes, int world,
                                  size_t flags_off, unsigned long long* ep, unsigned* arrive) {
   const unsigned long long e = ep[CH_HALO] + 1;
@@ -162,8 +162,8 @@ __global__ void peer_sum_kernel(double* vals, int n, PeerPtrs P, int me, int wor
 }
 
 // allgather push: my owned planes -> every rank's gather slot (same offset)
-__global__ void gather_push_kernel(const double* __restrict__ win, long long src_off, long long dst_off,
-                                   long long count, PeerPtrs P, int me, int world, size_t gather_off,
+__device__ __forceinline__ void gather_push(const double* __restrict__ win, long long src_off, long long dst_off,
+                                   long long count, const PeerPtrs& P, int me, int world, size_t gather_off,
                                    size_t gather_bytes, size_t flags_off, unsigned long long* ep,
                                    unsigned* arrive) {
   const unsigned long long e = ep[CH_GATHER] + 1;
@@ -179,7 +179,7 @@ __global__ void gather_push_kernel(const double* __restrict__ win, long long src
       st_rel_sys(reinterpret_cast<unsigned long long*>(P.base[r] + flags_off) + 3 * world + me, e);
 }
 
-__global__ void gather_pull_kernel(double* __restrict__ full, long long n, PeerPtrs P, int me,
+__device__ __forceinline__ void gather_pull(double* __restrict__ full, long long n, const PeerPtrs& P, int me,
                                    int world, size_t gather_off, size_t gather_bytes,
                                    size_t flags_off, unsigned long long* ep, unsigned* arrive) {
   const unsigned long long e = ep[CH_GATHER] + 1;
@@ -194,8 +194,29 @@ __global__ void gather_pull_kernel(double* __restrict__ full, long long n, PeerP
   if (last_block(arrive) && threadIdx.x == 0) ep[CH_GATHER] = e;
 }
 
+// One launch per exchange: the push, then (every block, once its own part is
+// stored) the wait for the peers' flags and the pull.  Blocks that finished
+// pushing spin on peer flags, so the grid must be co-resident: at most one
+// block per SM (xfer_blocks).  The epoch is read by every block before the last
+// block of the pull advances it (that block is last only after all arrived).
+template <class T>
+__global__ void halo_xchg_kernel(Xfer S, Xfer R, T* __restrict__ vec, PeerPtrs P, int me,
+                                 size_t slot_level_off, size_t slot_bytes, int world,
+                                 size_t flags_off, unsigned long long* ep, unsigned* arrive) {
+  halo_push<T>(S, vec, P, me, slot_level_off, slot_bytes, world, flags_off, ep, arrive);
+  halo_pull<T>(R, vec, P, me, slot_level_off, slot_bytes, world, flags_off, ep, arrive + 1);
+}
+__global__ void gather_xchg_kernel(const double* __restrict__ win, long long src_off, long long dst_off,
+                                   long long count, double* __restrict__ full, long long nfull,
+                                   PeerPtrs P, int me, int world, size_t gather_off,
+                                   size_t gather_bytes, size_t flags_off, unsigned long long* ep,
+                                   unsigned* arrive) {
+  gather_push(win, src_off, dst_off, count, P, me, world, gather_off, gather_bytes, flags_off, ep, arrive);
+  gather_pull(full, nfull, P, me, world, gather_off, gather_bytes, flags_off, ep, arrive + 1);
+}
+
 int xfer_blocks(long long n) {
-  return int(std::max<long long>(1, std::min<long long>((n + 255) / 256, 2 * num_sms())));
+  return int(std::max<long long>(1, std::min<long long>((n + 255) / 256, num_sms())));
 }
 
 }  // namespace
@@ -354,23 +375,15 @@ struct PeerComm {
     if (world == 1) return;  // no ghost planes: nothing to move
     const Xfer& ps = push[level];
     const Xfer& pl = pull[level];
-    if (eb == 8) {
-      halo_push_kernel<unsigned long long><<<xfer_blocks(ps.total), 256, 0, s>>>(
-          ps, static_cast<const unsigned long long*>(vec), P, rank, off_halo[level], slot_bytes[level],
+    const long long nmax = std::max(ps.total, pl.total);
+    if (eb == 8)
+      halo_xchg_kernel<unsigned long long><<<xfer_blocks(nmax), 256, 0, s>>>(
+          ps, pl, static_cast<unsigned long long*>(vec), P, rank, off_halo[level], slot_bytes[level],
           world, off_flags, ep.p, arrive.p);
-      SG_CHECK_LAUNCH();
-      halo_pull_kernel<unsigned long long><<<xfer_blocks(pl.total), 256, 0, s>>>(
-          pl, static_cast<unsigned long long*>(vec), P, rank, off_halo[level], slot_bytes[level], world,
-          off_flags, ep.p, arrive.p + 1);
-    } else {
-      halo_push_kernel<unsigned><<<xfer_blocks(ps.total), 256, 0, s>>>(
-          ps, static_cast<const unsigned*>(vec), P, rank, off_halo[level], slot_bytes[level], world,
+    else
+      halo_xchg_kernel<unsigned><<<xfer_blocks(nmax), 256, 0, s>>>(
+          ps, pl, static_cast<unsigned*>(vec), P, rank, off_halo[level], slot_bytes[level], world,
           off_flags, ep.p, arrive.p);
-      SG_CHECK_LAUNCH();
-      halo_pull_kernel<unsigned><<<xfer_blocks(pl.total), 256, 0, s>>>(
-          pl, static_cast<unsigned*>(vec), P, rank, off_halo[level], slot_bytes[level], world,
-          off_flags, ep.p, arrive.p + 1);
-    }
     SG_CHECK_LAUNCH();
   }
 
@@ -393,12 +406,9 @@ struct PeerComm {
       SG_CUDA(cudaMemcpyAsync(full + dst, win_vec + src, size_t(cnt) * 8, cudaMemcpyDeviceToDevice, s));
       return;
     }
-    gather_push_kernel<<<xfer_blocks(cnt), 256, 0, s>>>(win_vec, src, dst, cnt, P, rank, world,
-                                                        off_gather, gather_bytes, off_flags, ep.p,
-                                                        arrive.p + 2);
-    SG_CHECK_LAUNCH();
-    gather_pull_kernel<<<xfer_blocks(nfull), 256, 0, s>>>(full, nfull, P, rank, world, off_gather,
-                                                          gather_bytes, off_flags, ep.p, arrive.p + 3);
+    gather_xchg_kernel<<<xfer_blocks(std::max(cnt, nfull)), 256, 0, s>>>(
+        win_vec, src, dst, cnt, full, nfull, P, rank, world, off_gather, gather_bytes, off_flags,
+        ep.p, arrive.p + 2);
     SG_CHECK_LAUNCH();
   }
 };
