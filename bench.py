@@ -196,13 +196,22 @@ def run_gpu(args):
     import torch
 
     world, rank, local = _dist()
+    # development knob: SG_BENCH_ONE_DEVICE=1 runs every rank on cuda:0 over
+    # gloo (the multi-rank path on a one-GPU box; the peer transport maps the
+    # other processes' mailboxes through IPC on the same device)
+    one_dev = os.environ.get("SG_BENCH_ONE_DEVICE") == "1"
+    if one_dev:
+        local = 0
     torch.cuda.set_device(local)
     use_slab = world > 1 or args.slab
     if use_slab:
         import torch.distributed as dist
         if "MASTER_ADDR" not in os.environ:  # --slab on one process without torchrun
             os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT="29533", RANK="0", WORLD_SIZE="1")
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if one_dev:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     import paper_2604_26441_b200 as P
     from paper_2604_26441_b200 import _dev, _native
 
@@ -303,7 +312,7 @@ def run_gpu(args):
     torch.cuda.synchronize()
     ms = total_ms / args.steps
     if world > 1:
-        t = torch.tensor([ms], device="cuda", dtype=torch.float64)
+        t = torch.tensor([ms], device="cpu" if one_dev else "cuda", dtype=torch.float64)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         ms = float(t.item())
         torch.distributed.barrier()
@@ -357,7 +366,7 @@ def run_gpu(args):
     import statistics
     e2e_s = statistics.median(e2e)
     if world > 1:
-        t = torch.tensor([e2e_s], device="cuda", dtype=torch.float64)
+        t = torch.tensor([e2e_s], device="cpu" if one_dev else "cuda", dtype=torch.float64)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         e2e_s = float(t.item())
     e2e_detail = {"samples": len(e2e), "median_s": e2e_s, "min_s": min(e2e), "max_s": max(e2e),
@@ -374,7 +383,8 @@ def run_gpu(args):
     if os.path.exists(tpath):
         try:
             tj = json.load(open(tpath))
-            traffic, traffic_src = tj.get("fine_apply_fp32_bytes"), tj.get("source")
+            if N == 100:  # the capture is of the 100^3 launch
+                traffic, traffic_src = tj.get("fine_apply_fp32_bytes"), tj.get("source")
         except Exception:
             traffic = None
     line = {
