@@ -121,7 +121,7 @@ fine_bf16_tc2_kernel(GridDesc g, const uint8_t* __restrict__ nmask, const float*
 
   // ---- this thread's element slots: tiles m = (warp >> 2) + 4 a, row 32 (warp & 3) + lane
   const int q4 = warp & 3, m0 = warp >> 2;
-  constexpr int kA = kT2MaxTiles / (kT2Threads / 128);  // tiles per thread (2)
+  constexpr int kA = (kT2MaxTiles + kT2Threads / 128 - 1) / (kT2Threads / 128);  // tiles per thread
   int tt[kA], eo[kA];       // slot, element offset in its layer (-1: no element)
   bool ownn[kA];
   int64_t onode[kA];
