@@ -277,7 +277,7 @@ static void smooth_p32(Hier& H, Level& L, const double* b64, const double* x0, d
     }
   }
   L.w.xcur = x;
-  if (!out_done) from_p32<double>(g, x, out, s);
+  if (!out_done && out) from_p32<double>(g, x, out, s);
 }
 
 // fused FP64 stencil Chebyshev step / residual on the symmetric copy when
@@ -373,7 +373,16 @@ void cycle(Hier& H, int l, int gamma, cudaStream_t s) {
   const int64_t n = L.nd();
   // pre-smoothing writes x (f64) into w.d64 scratch first, then moved to w.x
   double* x64 = L.w.d64.p;  // holds the f64 iterate across the coarse visits
-  level_smooth(H, l, L.w.r.p, nullptr, x64, s);
+  // V-cycle on a P32 level (one coarse visit, no slab tail below): the f64
+  // iterate is never needed as such -- it is f64(x32) exactly before the
+  // correction, and the post-smoother starts from f32(x + P e) -- so it is
+  // not materialised: the pre-smoother skips its f64 output and the
+  // prolongation adds onto f64(x32) in place (SG_P32_X64=1 restores it)
+  static const bool keep64 = std::getenv("SG_P32_X64") != nullptr;
+  const bool no64 = L.p32 && gamma == 1 && !keep64 && !(H.dist && l + 1 == H.dist->n_dist) &&
+                    !std::getenv("SG_P32_UNFUSED");
+  if (no64) smooth_p32(H, L, L.w.r.p, nullptr, nullptr, s);
+  else level_smooth(H, l, L.w.r.p, nullptr, x64, s);
   for (int g = 0; g < gamma; ++g) {
     if (L.tag == TAG_FP64 && !L.is_fine && !std::getenv("SG_ST64_UNFUSED")) {
       if (H.comm) H.comm->exchange(l, x64, 8, s);
@@ -405,8 +414,14 @@ void cycle(Hier& H, int l, int gamma, cudaStream_t s) {
       restrict_(*L.g, *C.g, L.w.x.p, C.w.r.p, s);  // L.w.x used as residual scratch here
       cycle(H, l + 1, gamma, s);
       if (H.comm) H.comm->exchange(l + 1, C.w.x.p, 8, s);  // prolongation reads ghost corrections
-      if (L.p32)  // also writes f32(x64) into x32 (P32) for the post-smoother
-        prolong(*L.g, *C.g, C.w.x.p, x64, /*add=*/true, s, L.w.x32.p, p32_xs(L.g->d));
+      if (L.p32) {
+        // also writes f32(x64) into x32 (P32) for the post-smoother; without
+        // the f64 iterate (no64) it adds onto f64(x32) and writes x32 only
+        // the iterate may sit in the ping-pong partner: swap the two buffers'
+        // roles (a host pointer swap, fixed in the captured graph)
+        if (no64 && L.w.xcur != L.w.x32.p) std::swap(L.w.x32, L.w.x32b);
+        prolong(*L.g, *C.g, C.w.x.p, no64 ? nullptr : x64, /*add=*/true, s, L.w.x32.p, p32_xs(L.g->d));
+      }
       else
         prolong(*L.g, *C.g, C.w.x.p, x64, /*add=*/true, s);
     }

@@ -38,6 +38,15 @@ __global__ void prolong_kernel(GridDesc f, GridDesc c, const uint8_t* __restrict
       }
 #pragma unroll
   for (int ax = 0; ax < 3; ++ax) {
+    float* o32 = xp32 ? xp32 + ((int64_t(k) * FY + j) * 3 + ax) * XS + i : nullptr;
+    if (!xf) {
+      // V-cycle on a P32 level: the f64 iterate is f64(x32) exactly, so the
+      // sum is formed from the P32 copy and only f32(x + P e) is stored
+      const double base = double(*o32);
+      const double v = node_fixed_axis(f, fmask, node, i, ax) ? base : __dadd_rn(base, s[ax]);
+      *o32 = __double2float_rn(v);
+      continue;
+    }
     double* o = xf + 3 * node + ax;
     double v;
     if (node_fixed_axis(f, fmask, node, i, ax)) {
@@ -48,7 +57,7 @@ __global__ void prolong_kernel(GridDesc f, GridDesc c, const uint8_t* __restrict
       *o = v;
     }
     // level-0 P32 copy f32(x) for the post-smoother (sg_fine_pk.cu layout)
-    if (xp32) xp32[((int64_t(k) * FY + j) * 3 + ax) * XS + i] = __double2float_rn(v);
+    if (o32) *o32 = __double2float_rn(v);
   }
 }
 
