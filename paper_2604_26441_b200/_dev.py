@@ -71,8 +71,17 @@ def zeros(n, dtype=np.float64):
     return torch.zeros(int(n), dtype=tdt, device=device())
 
 
+_PINNED_MIN = 1 << 20
+
+
 def back(t, host):
-    """Return numpy (for host callers) or the device tensor."""
+    """Return numpy (for host callers) or the device tensor.  Large results are
+    copied into page-locked memory (torch's caching host allocator) so the D2H
+    runs at the full link rate; the numpy array keeps that buffer alive."""
     if host:
+        if t.numel() * t.element_size() >= _PINNED_MIN:
+            out = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+            out.copy_(t)
+            return out.numpy()
         return t.cpu().numpy()
     return t
