@@ -428,7 +428,8 @@ void cycle(Hier& H, int l, int gamma, cudaStream_t s) {
     L.w.xcur = nullptr;  // x64 changed: a W-cycle's next residual re-converts
   }
   if (L.p32) {
-    smooth_p32(H, L, L.w.r.p, x64, L.w.x.p, s, /*b_ready=*/true, /*x0_ready=*/true);
+    smooth_p32(H, L, L.w.r.p, x64, (l == 0 && H.skip_z64) ? nullptr : L.w.x.p, s,
+               /*b_ready=*/true, /*x0_ready=*/true);
     return;
   }
   level_smooth(H, l, L.w.r.p, x64, L.w.x.p, s);
@@ -437,6 +438,50 @@ void cycle(Hier& H, int l, int gamma, cudaStream_t s) {
 Hier::~Hier() {
   for (auto& g : graph)
     if (g) cudaGraphExecDestroy(g);
+  if (graph_noz) cudaGraphExecDestroy(graph_noz);
+}
+
+const float* cycle_run_noz(Hier& H, cudaStream_t s) {
+  SG_REQUIRE(!H.released && H.lv[0]->p32 && !H.dist, "z-in-P32 cycle needs a P32 level 0");
+  if (std::getenv("SG_NO_GRAPH")) {
+    H.skip_z64 = true;
+    try {
+      cycle(H, 0, 1, s);
+    } catch (...) {
+      H.skip_z64 = false;
+      throw;
+    }
+    H.skip_z64 = false;
+    return H.lv[0]->w.xcur;
+  }
+  if (!H.graph_noz) {
+    cudaStream_t cs = nullptr;
+    SG_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+    cudaGraph_t g = nullptr;
+    SG_CUDA(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+    H.skip_z64 = true;
+    try {
+      cycle(H, 0, 1, cs);
+    } catch (...) {
+      H.skip_z64 = false;
+      cudaStreamEndCapture(cs, &g);
+      if (g) cudaGraphDestroy(g);
+      cudaStreamDestroy(cs);
+      throw;
+    }
+    H.skip_z64 = false;
+    H.zcur32 = H.lv[0]->w.xcur;  // the buffer the captured post-smoother ends in
+    SG_CUDA(cudaStreamEndCapture(cs, &g));
+    cudaStreamDestroy(cs);
+    size_t n = 0;
+    SG_CUDA(cudaGraphGetNodes(g, nullptr, &n));
+    SG_CUDA(cudaGraphInstantiate(&H.graph_noz, g, 0));
+    SG_CUDA(cudaGraphDestroy(g));
+    H.graph_noz_nodes = n;
+  }
+  SG_CUDA(cudaGraphLaunch(H.graph_noz, s));
+  __atomic_add_fetch(&g_sg_launches, (unsigned long long)H.graph_noz_nodes, __ATOMIC_RELAXED);
+  return H.zcur32;
 }
 
 void cycle_run(Hier& H, int gamma, cudaStream_t s) {
@@ -779,6 +824,10 @@ void dist_release_full(DistPart& D, cudaStream_t s) {
       cudaGraphExecDestroy(g);
       g = nullptr;
     }
+  if (F.graph_noz) {
+    cudaGraphExecDestroy(F.graph_noz);
+    F.graph_noz = nullptr;
+  }
   F.io_a.release();
   F.io_b.release();
   D.full_released = true;

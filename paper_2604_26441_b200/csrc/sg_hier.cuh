@@ -93,11 +93,20 @@ struct Hier {
   const CommHooks* comm = nullptr;  // slab windows: halo before every level apply
   DistPart* dist = nullptr;         // slab windows: the part (coarse-tail transition)
   bool released = false;  // slab levels freed for a slab solve (dist_release_full)
+  // V-cycle variant for the native PCG on a P32 level: the final f64 output z is
+  // not written (z = f64 of the FP32 iterate, read from P32 by rz_pupd)
+  bool skip_z64 = false;
+  cudaGraphExec_t graph_noz = nullptr;
+  size_t graph_noz_nodes = 0;
+  const float* zcur32 = nullptr;  // the noz graph's final FP32 iterate (P32 layout)
   ~Hier();
 };
 // One V/W-cycle from lv[0]->w.r into lv[0]->w.x, replayed from a CUDA graph
 // captured on first use (set SG_NO_GRAPH=1 to launch kernel by kernel).
 void cycle_run(Hier& H, int gamma, cudaStream_t s);
+// V-cycle without the f64 output (level 0 in the P32 layout): returns the P32
+// buffer holding z in FP32 (z_f64 = f64 of it exactly)
+const float* cycle_run_noz(Hier& H, cudaStream_t s);
 
 // Device scratch of the native solvers, allocated on first use and reused by
 // every later solve (no cudaMalloc/cudaFree -- and their implicit device

@@ -251,6 +251,43 @@ __global__ void __launch_bounds__(kRedThreads, 8) rz_pupd_kernel(int64_t n, int6
   for (int64_t i = i0; i < nd; i += stride) p[i] = __dadd_rn(z[i], __dmul_rn(beta, p[i]));  // pupd
 }
 
+// rz_pupd with z read from the V-cycle's FP32 iterate in the P32 layout
+// (sg_fine_pk.cu): z_f64 = f64 of it exactly, so r.z and p = z + beta p carry
+// the bits of the node-layout path while the f64 z is never written or read.
+struct ZP32 {
+  const float* z32;
+  int NX, XS;
+  __device__ __forceinline__ double operator()(int64_t d) const {
+    const int d32 = int(d), node = d32 / 3, c = d32 - 3 * node;
+    const int jk = node / NX, i = node - jk * NX;
+    return double(z32[(jk * 3 + c) * XS + i]);
+  }
+};
+__global__ void __launch_bounds__(kRedThreads, 8) rz_pupd_z32_kernel(int64_t n, ZP32 Z,
+                                                                  const double* __restrict__ r,
+                                                                  double* __restrict__ p, double* sc,
+                                                                  double* partials,
+                                                                  unsigned long long* bar) {
+  __shared__ double smem[8];
+  __shared__ double bc;
+  const int64_t stride = int64_t(gridDim.x) * kRedThreads;
+  const int64_t i0 = int64_t(blockIdx.x) * kRedThreads + threadIdx.x;
+  double acc[1] = {0.0};
+  for (int64_t i = i0; i < n; i += stride) acc[0] = fma(r[i], Z(i), acc[0]);  // Dot
+  block_sum<1>(acc, smem);
+  if (threadIdx.x == 0) partials[blockIdx.x] = acc[0];
+  const double rz_old = sc[S_RZ];
+  grid_barrier(bar);
+  const double t = sum_partials(partials, smem, &bc);
+  const double beta = __ddiv_rn(t, rz_old);  // RznPost
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    sc[S_RZN] = t;
+    sc[S_BETA] = beta;
+    sc[S_RZ] = t;
+  }
+  for (int64_t i = i0; i < n; i += stride) p[i] = __dadd_rn(Z(i), __dmul_rn(beta, p[i]));  // pupd
+}
+
 struct View {  // non-owning handle on a reused SolverWork buffer
   double* p;
 };
@@ -309,10 +346,11 @@ struct Ctx {
     static int per_sm = -1;
     if (!psum_ok || std::getenv("SG_PCG_UNFUSED")) return 0;
     if (per_sm < 0) {
-      int a = 0, b = 0;
+      int a = 0, b = 0, c = 0;
       SG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a, pq_step_kernel, kRedThreads, 0));
       SG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, rz_pupd_kernel, kRedThreads, 0));
-      per_sm = std::min(a, b);
+      SG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c, rz_pupd_z32_kernel, kRedThreads, 0));
+      per_sm = std::min(a, std::min(b, c));
     }
     const int nb = red_blocks(nown);
     return nb <= per_sm * num_sms() ? nb : 0;
@@ -341,6 +379,24 @@ struct Ctx {
     PeerSumDev ps = psum;
     void* args[] = {&n, &ndd, &o, &r, &z, &p, &scp, &part, &bar, &ps};
     SG_CUDA(cudaLaunchCooperativeKernel((const void*)rz_pupd_kernel, dim3(nb), dim3(kRedThreads), args, 0, s));
+    SG_CHECK_LAUNCH();
+  }
+  // one GPU, P32 level 0, V-cycle, fused kernels: z stays in FP32 / P32
+  bool z32_ok() {
+    return sys.hier && !sys.dist && sys.gamma == 1 && sys.hier->lv[0]->p32 && fused_blocks() &&
+           !std::getenv("SG_PCG_Z64");
+  }
+  void M_rz_pupd_z32(const double* r, double* p) {
+    Level& L0 = *sys.hier->lv[0];
+    if (r != L0.w.r.p) copy_k<<<nb256(nd), 256, 0, s>>>(nd, r, L0.w.r.p);
+    ZP32 Z{cycle_run_noz(*sys.hier, s), L0.g->d.nx + 1, p32_xs(L0.g->d)};
+    int64_t n = nd;
+    double* scp = sc.p;
+    double* part = red.partials.p;
+    unsigned long long* bar = red.gbar.p;
+    void* args[] = {&n, &Z, &r, &p, &scp, &part, &bar};
+    SG_CUDA(cudaLaunchCooperativeKernel((const void*)rz_pupd_z32_kernel, dim3(fused_blocks()),
+                                        dim3(kRedThreads), args, 0, s));
     SG_CHECK_LAUNCH();
   }
   // z = apply_M(r)
@@ -469,8 +525,9 @@ void pcg_native(NativeSys& sys, const double* b, double* x, const SolverCfg& cfg
       }
       target *= 0.1;
     }
-    C.M(r, z.p);
-    if (const int fb = C.fused_blocks()) {
+    if (C.z32_ok()) {
+      C.M_rz_pupd_z32(r, p.p);  // z never materialised in f64 (same bits)
+    } else if (const int fb = (C.M(r, z.p), C.fused_blocks())) {
       C.rz_pupd(r, z.p, p.p, fb);
     } else {
       C.reduce(Dot{r + C.off, z.p + C.off}, RznPost{C.sc.p}, S_TMP);
