@@ -170,6 +170,7 @@ fine_p64_kernel(GridDesc g, const uint8_t* __restrict__ nmask, const double* __r
   load_plane(k0 + 1);
   __syncthreads();
   plane_q(0, QA);
+  __syncthreads();  // buffer 0 is refilled by the first layer's store_plane
 #pragma unroll
   for (int c = 0; c < 3; ++c)
 #pragma unroll

@@ -336,7 +336,10 @@ fine_bf16_tc2_kernel(GridDesc g, const uint8_t* __restrict__ nmask, const float*
       asm volatile("bar.arrive 1, %0;" ::"n"(kT2Block) : "memory");
       // D: epilogue of the previous layer while layer ek's MMAs run
       if (ek > k0 - 1) epilogue(ek - 1);
-      // C: stage node plane ek+3 (buffer of plane ek, recorded last layer)
+      // C: stage node plane ek+3 into the buffer of plane ek (recorded last
+      // layer; in the first layer by the prologue, with no epilogue barrier
+      // since -- wait for every thread's reads of it first)
+      if (ek == k0 - 1) asm volatile("bar.sync 3, %0;" ::"n"(kT2Threads) : "memory");
       stage(ek + 3);
       asm volatile("cp.async.wait_group 1;" ::: "memory");  // plane ek+2 landed
       asm volatile("bar.sync 3, %0;" ::"n"(kT2Threads) : "memory");

@@ -688,6 +688,7 @@ std::unique_ptr<Hier> hier_build(FineOp* fine, FineWork& fw, const HParams& p, c
     if (L.p32) {  // dinv32 in the P32 layout (0 on padding); the node-layout
                   // copy stays for the slab windows (dist_build)
       L.dinv32p.alloc(size_t(L.n32()));
+      L.dinv32p.zero(s);  // the P32 slack past the last plane is never written
       to_p32<float>(L.g->d, L.dinv32.p, L.dinv32p.p, s);
     }
     alloc_work(L, s);
@@ -937,6 +938,7 @@ std::unique_ptr<DistPart> dist_build(Hier& F, int n_dist, const int* planes, con
     SG_CUDA(cudaMemcpyAsync(L->dinv32.p, FL.dinv32.p + voff, sizeof(float) * n, cudaMemcpyDeviceToDevice, s));
     if (L->p32) {
       L->dinv32p.alloc(size_t(L->n32()));
+      L->dinv32p.zero(s);
       to_p32<float>(L->g->d, L->dinv32.p, L->dinv32p.p, s);
     }
     alloc_work(*L, s);
