@@ -525,9 +525,11 @@ void pcg_native(NativeSys& sys, const double* b, double* x, const SolverCfg& cfg
       }
       target *= 0.1;
     }
-    if (C.z32_ok()) {
+    const bool z32 = C.z32_ok();
+    if (!z32) C.M(r, z.p);
+    if (z32) {
       C.M_rz_pupd_z32(r, p.p);  // z never materialised in f64 (same bits)
-    } else if (const int fb = (C.M(r, z.p), C.fused_blocks())) {
+    } else if (const int fb = C.fused_blocks()) {
       C.rz_pupd(r, z.p, p.p, fb);
     } else {
       C.reduce(Dot{r + C.off, z.p + C.off}, RznPost{C.sc.p}, S_TMP);

@@ -22,6 +22,7 @@
 // epochs live in device memory and advance inside the kernels: graph replays
 // stay in step.  Sums are accumulated in rank order: identical bits on every
 // rank, as TorchSlabComm.allreduce.
+#include <cstdio>
 #include <cstring>
 #include "sg_hier.cuh"
 #include "sg_peer.cuh"
@@ -414,29 +415,34 @@ struct PeerComm {
 };
 
 namespace {
-int hook_halo(void* ctx, int level, void* vec, int eb, void* stream) {
+// the hooks cross a C function-pointer boundary: report failures by status,
+// with the reason on stderr (CommHooks then raises "slab ... failed")
+template <class F>
+int hook_call(const char* what, F&& f) {
   try {
-    static_cast<PeerComm*>(ctx)->halo(level, vec, eb, static_cast<cudaStream_t>(stream));
+    f();
     return 0;
+  } catch (const std::exception& e) {
+    fprintf(stderr, "peer transport %s: %s\n", what, e.what());
   } catch (...) {
-    return 1;
+    fprintf(stderr, "peer transport %s: unknown error\n", what);
   }
+  return 1;
+}
+int hook_halo(void* ctx, int level, void* vec, int eb, void* stream) {
+  return hook_call("halo", [&] {
+    static_cast<PeerComm*>(ctx)->halo(level, vec, eb, static_cast<cudaStream_t>(stream));
+  });
 }
 int hook_sum(void* ctx, double* vals, int n, void* stream) {
-  try {
+  return hook_call("sum", [&] {
     static_cast<PeerComm*>(ctx)->sum(vals, n, static_cast<cudaStream_t>(stream));
-    return 0;
-  } catch (...) {
-    return 1;
-  }
+  });
 }
 int hook_gather(void* ctx, int level, const double* win, double* full, void* stream) {
-  try {
+  return hook_call("gather", [&] {
     static_cast<PeerComm*>(ctx)->gather(level, win, full, static_cast<cudaStream_t>(stream));
-    return 0;
-  } catch (...) {
-    return 1;
-  }
+  });
 }
 }  // namespace
 
