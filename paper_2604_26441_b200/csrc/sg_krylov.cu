@@ -6,6 +6,7 @@
 // vector operation and reduction runs on the device, deterministically.
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include "sg_hier.cuh"
 #include "sg_peer.cuh"
 
@@ -135,17 +136,41 @@ inline int nb256(int64_t n) { return grid_blocks(n, 256); }
 // here by every block after a grid barrier instead of by the last block), so
 // the results are bit-identical to the separate launches (and to the slab
 // path with one rank).  Cooperative launch guarantees co-residency.
+// Barrier: thread 0 of each block arrives with a gpu-scope release add and
+// polls with acquire loads (the bar.sync on either side orders the block's
+// other threads); c_fence_bar = 1 (SG_PCG_FENCE_BAR=1) restores the round-1
+// form with two full fences and a __nanosleep back-off.
+__constant__ int c_fence_bar;
 __device__ __forceinline__ void grid_barrier(unsigned long long* ctr) {
   __syncthreads();
   if (threadIdx.x == 0) {
-    __threadfence();
     const unsigned long long nb = gridDim.x;
-    const unsigned long long old = atomicAdd(ctr, 1ull);
-    const unsigned long long target = (old / nb + 1) * nb;  // counter grows by nb per launch
-    while (*(volatile unsigned long long*)ctr < target) __nanosleep(32);
-    __threadfence();
+    if (c_fence_bar) {
+      __threadfence();
+      const unsigned long long old = atomicAdd(ctr, 1ull);
+      const unsigned long long target = (old / nb + 1) * nb;  // counter grows by nb per launch
+      while (*(volatile unsigned long long*)ctr < target) __nanosleep(32);
+      __threadfence();
+    } else {
+      unsigned long long old, v;
+      asm volatile("atom.add.release.gpu.global.u64 %0, [%1], 1;" : "=l"(old) : "l"(ctr) : "memory");
+      const unsigned long long target = (old / nb + 1) * nb;
+      do {
+        asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(ctr) : "memory");
+      } while (v < target);
+    }
   }
   __syncthreads();
+}
+// last-block election: release of this block's partial, acquire of the others'
+__device__ __forceinline__ bool arrive_last(unsigned* counter) {
+  if (c_fence_bar) {
+    __threadfence();
+    return atomicAdd(counter, 1u) == gridDim.x - 1;
+  }
+  unsigned old;
+  asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], 1;" : "=r"(old) : "l"(counter) : "memory");
+  return old == gridDim.x - 1;
 }
 // every block: the reduce_kernel last-block sum of partials[0..gridDim)
 __device__ __forceinline__ double sum_partials(const double* partials, double* smem, double* bc) {
@@ -203,12 +228,11 @@ __global__ void __launch_bounds__(kRedThreads, 8) pq_step_kernel(int64_t n, doub
   double* part2 = partials + gridDim.x;  // phase-1 partials may still be being read
   if (threadIdx.x == 0) {
     part2[blockIdx.x] = acc2[0];
-    __threadfence();
-    last = atomicAdd(counter, 1u) == gridDim.x - 1;
+    last = arrive_last(counter);
   }
   __syncthreads();
   if (!last) return;
-  __threadfence();
+  if (c_fence_bar) __threadfence();
   double rr = sum_partials(part2, smem, &bc);
   if (threadIdx.x == 0) {  // PcgStepPost, from the values in registers
     if (ps.world > 1) rr = peer_sum1(ps, rr);
@@ -317,6 +341,14 @@ struct Ctx {
       nown = sys.dist->own_n(0);
     }
     red.init(s);
+    static const bool fence_bar = [] {  // A/B switch of the grid barrier form (read once)
+      if (std::getenv("SG_PCG_FENCE_BAR")) {
+        const int one = 1;
+        SG_CUDA(cudaMemcpyToSymbol(c_fence_bar, &one, sizeof(int)));
+      }
+      return true;
+    }();
+    (void)fence_bar;
     if (!sc.p) sc.alloc(256);
     SG_CUDA(cudaMemsetAsync(sc.p, 0, 256 * sizeof(double), s));
     if (sys.ktag != TAG_FP64 && t32a.n < size_t(nd)) {
