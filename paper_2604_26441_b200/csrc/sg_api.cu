@@ -799,6 +799,12 @@ extern "C" int sg_hier_profile(sg_hier* h, int what, int reps, double* ms_avg, v
     double total = 0.0;
     for (int r = 0; r < reps; ++r) {
       SG_CUDA(cudaMemsetAsync(flush.p, r & 0xff, flush.n, s));
+      // 8 / 9: the coarsest solve right after another coarsest solve / after the
+      // restriction onto the coarsest level (launch-transition cost probes)
+      if (what == 8) sg::coarsest_solve(H, H.lv.back()->w.r.p, H.lv.back()->w.x.p, s);
+      if (what == 9 && H.lv.size() > 1)
+        sg::restrict_(*H.lv[H.lv.size() - 2]->g, *H.lv.back()->g, H.lv[H.lv.size() - 2]->w.r.p,
+                      H.lv.back()->w.r.p, s);
       SG_CUDA(cudaEventRecord(e0, s));
       switch (what) {
         case 0:  // the level-0 FP32 apply the V-cycle runs (P32 layout when supported)
@@ -816,7 +822,9 @@ extern "C" int sg_hier_profile(sg_hier* h, int what, int reps, double* ms_avg, v
             sg::stencil_apply<double>(*L1.g, L1.st.T64.p, L1.w.r.p, L1.w.y64.p, s);
           break;
         }
-        case 3: {
+        case 3:
+        case 8:
+        case 9: {
           sg::Level& Lc = *H.lv.back();
           sg::coarsest_solve(H, Lc.w.r.p, Lc.w.x.p, s);
           break;
