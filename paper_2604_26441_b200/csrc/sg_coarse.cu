@@ -692,9 +692,10 @@ __global__ void __launch_bounds__(br_threads(kVar), 1) pcg80_brick_kernel(BrickA
       constexpr int q0 = decltype(q0c)::value, nr = decltype(nrc)::value;
       constexpr int np = (nr * 9 + 1) / 2;
       double v[2 * np];
+      // (threads past the brick's nodes hold zero padding: not loaded)
 #pragma unroll
       for (int j = 0; j < np; ++j) {
-        const double2 d = __ldg(src + (q0 * 9 / 2 + j) * kBrBlock);
+        const double2 d = act ? __ldg(src + (q0 * 9 / 2 + j) * kBrBlock) : make_double2(0.0, 0.0);
         v[2 * j] = d.x;
         v[2 * j + 1] = d.y;
       }
