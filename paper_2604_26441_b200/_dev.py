@@ -54,6 +54,7 @@ def as_device(x, dtype=np.float64, n=None):
         t = t.contiguous().reshape(-1)
         host = False
     else:
+        dev = device()  # raises NativeError first on a box without a GPU
         a = np.ascontiguousarray(np.asarray(x), dtype=dtype).reshape(-1)
         src = torch.from_numpy(a)
         if a.nbytes >= _PINNED_MIN:
@@ -63,9 +64,9 @@ def as_device(x, dtype=np.float64, n=None):
             # driver's pageable path (24.5 MB: 1.22 -> 0.71 ms on the B200 box)
             pin = torch.empty(src.shape, dtype=src.dtype, pin_memory=True)
             pin.copy_(src)
-            t = pin.to(device(), non_blocking=True)
+            t = pin.to(dev, non_blocking=True)
         else:
-            t = src.to(device(), non_blocking=False)
+            t = src.to(dev, non_blocking=False)
         host = True
     if n is not None and t.numel() != n:
         raise ValueError(f"expected free vector of length {n}")
