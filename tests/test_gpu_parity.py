@@ -462,9 +462,13 @@ def test_fused_pcg_reductions_bit_identical():
         "    out[str(dims) + 'j'] = np.array(rj.residual_history)\n"
         "np.savez(sys.argv[1], **out)\n" % root)
     res = {}
-    for name, env in (("fused", {}), ("unfused", {"SG_PCG_UNFUSED": "1"})):
+    # (SG_PCG_FENCE_BAR=1: the cooperative kernels' round-1 fenced grid barrier
+    # instead of the release/acquire one -- synchronisation only, same bits)
+    for name, env in (("fused", {}), ("unfused", {"SG_PCG_UNFUSED": "1"}),
+                      ("fenced", {"SG_PCG_FENCE_BAR": "1"})):
         path = f"/tmp/_pcgf_{name}.npz"
         subprocess.run([sys.executable, "-c", code, path], check=True, env=dict(os.environ, **env))
         res[name] = np.load(path)
     for k in res["fused"].files:
         assert np.array_equal(res["fused"][k], res["unfused"][k]), k
+        assert np.array_equal(res["fused"][k], res["fenced"][k]), k
