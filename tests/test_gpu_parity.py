@@ -304,6 +304,31 @@ def test_fine_apply_fp64_block_tiling(dims, kind):
     assert np.array_equal(y, op.matvec_tagged(u, P.PrecisionTag.FP64))
 
 
+def test_fine_apply_fp64_block_size_bit_identical():
+    """The FP64 apply with its compile-time 512-thread block size equals the
+    runtime-block-size instantiation (SG_P64_RTNT=1) bit for bit."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = (
+        "import sys, numpy as np; sys.path.insert(0, %r)\n"
+        "import paper_2604_26441_b200 as P\n"
+        "out = {}\n"
+        "for dims, kind in (((100,100,100),'uniform'), ((131,7,5),'binary'), ((63,40,9),'random_floor')):\n"
+        "    g = P.build_cantilever(*dims)\n"
+        "    op = P.FineOperator(g, P.simp_modulus(P.make_state(kind, *dims, vf=0.5, seed=42), 3.0))\n"
+        "    out[str(dims)] = op.matvec_tagged(P.SplitMix64(5).gaussian(g.n_free), P.PrecisionTag.FP64)\n"
+        "np.savez(sys.argv[1], **out)\n" % root)
+    res = {}
+    for name, env in (("ct", {}), ("rt", {"SG_P64_RTNT": "1"})):
+        path = f"/tmp/_p64nt_{name}.npz"
+        subprocess.run([sys.executable, "-c", code, path], check=True, env=dict(os.environ, **env))
+        res[name] = np.load(path)
+    for k in res["ct"].files:
+        assert np.array_equal(res["ct"][k], res["rt"][k]), k
+
+
 @pytest.mark.parametrize("dims,kind", [((100, 100, 100), "uniform"), ((131, 7, 5), "binary"),
                                        ((9, 33, 17), "random_floor"), ((1, 1, 1), "uniform"),
                                        ((2, 61, 3), "binary"), ((200, 3, 2), "binary"),
