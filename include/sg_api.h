@@ -290,6 +290,9 @@ int sg_plan_brick(int nx, int ny, int nz, int nsm, int32_t* out3);
  * terminated (cap = max pieces). */
 int sg_plan_halo(int world, const int32_t* windows, int32_t* out, int cap);
 int sg_plan_p32(int nx, int ny, int nz, int nsm, int32_t* out7);
+/* sg_plan_p32 for an explicit block size nt (256: two CTAs per SM, the fused
+ * smoother / residual applies' default when R >= 5; 512: one CTA per SM). */
+int sg_plan_p32_bs(int nx, int ny, int nz, int nsm, int nt, int32_t* out7);
 
 #ifdef __cplusplus
 }

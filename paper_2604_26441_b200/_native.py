@@ -99,6 +99,7 @@ SIGNATURES = {
     "sg_hier_pcg80_trace": (c_int, [c_void_p, c_void_p, c_void_p]),
     "sg_plan_brick": (c_int, [c_int, c_int, c_int, c_int, c_void_p]),
     "sg_plan_p32": (c_int, [c_int, c_int, c_int, c_int, c_void_p]),
+    "sg_plan_p32_bs": (c_int, [c_int, c_int, c_int, c_int, c_int, c_void_p]),
     "sg_pcg": (c_int, [c_void_p, c_int, c_void_p, c_int, c_void_p, c_void_p, P(SolverCfg),
                        P(Report), c_void_p, c_void_p]),
     "sg_fgmres": (c_int, [c_void_p, c_int, c_void_p, c_int, c_void_p, c_void_p, P(SolverCfg),

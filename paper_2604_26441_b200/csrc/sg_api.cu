@@ -920,14 +920,22 @@ extern "C" int sg_plan_brick(int nx, int ny, int nz, int nsm, int32_t* out3) {
     out3[2] = ok ? sz : 0;
   });
 }
-extern "C" int sg_plan_p32(int nx, int ny, int nz, int nsm, int32_t* out7) {
+extern "C" int sg_plan_p32_bs(int nx, int ny, int nz, int nsm, int nt, int32_t* out7) {
   return guard([&] {
+    SG_REQUIRE(nt == 256 || nt == 512, "sg_plan_p32_bs: block size 256 or 512");
     sg::GridDesc g;
     g.nx = nx;
     g.ny = ny;
     g.nz = nz;
-    const sg::PkPlan pl = sg::pk_plan(g, nsm);
+    const sg::PkPlan pl = sg::pk_plan(g, nsm, nt);
     const int v[7] = {pl.P, pl.T, pl.SX, pl.R, pl.tilesy, pl.kchunk, pl.nch};
     for (int i = 0; i < 7; ++i) out7[i] = v[i];
   });
+}
+extern "C" int sg_plan_p32(int nx, int ny, int nz, int nsm, int32_t* out7) {
+  sg::GridDesc g;
+  g.nx = nx;
+  g.ny = ny;
+  g.nz = nz;
+  return sg_plan_p32_bs(nx, ny, nz, nsm, sg::pk_threads(g, 0), out7);
 }

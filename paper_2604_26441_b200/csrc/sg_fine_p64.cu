@@ -73,8 +73,11 @@ static bool pk64_params(const FineOp& op, PkCoefD& C) {
   return true;
 }
 
+// NT: compile-time block size (0: runtime); 256-thread blocks run two CTAs
+// per SM (NT = 256 -> __launch_bounds__(256, 2))
+constexpr int p64_bs(int nt) { return nt > 0 ? nt : kP64MaxThreads; }
 template <int LD, int NT>
-__global__ void __launch_bounds__(kP64MaxThreads, 1)
+__global__ void __launch_bounds__(p64_bs(NT), kP64MaxThreads / p64_bs(NT))
 fine_p64_kernel(GridDesc g, const uint8_t* __restrict__ nmask, const double* __restrict__ u,
                 double* __restrict__ yout, const double* __restrict__ E, PkCoefD C, int W, int R,
                 int kchunk) {
@@ -285,15 +288,16 @@ fine_p64_kernel(GridDesc g, const uint8_t* __restrict__ nmask, const double* __r
 struct P64Plan {
   int W = 0, R = 0, tx = 0, ty = 0, kchunk = 0, nch = 0;
 };
-static P64Plan p64_plan(const GridDesc& g, int nsm) {
+static P64Plan p64_plan(const GridDesc& g, int nsm, int maxt = kP64MaxThreads) {
   const int NX = g.nx + 1, NY = g.ny + 1, planes = g.nz + 1;
+  nsm *= kP64MaxThreads / maxt;  // resident CTAs per wave
   P64Plan best;
   double best_cost = 1e300;
   for (int T = 1; T <= 16; ++T) {
     const int own_x = (NX + T - 1) / T;
     const int W = own_x + 1;
-    if (W > kP64MaxThreads / 2 || own_x < std::min(NX, 15)) continue;
-    const int R = std::min(kP64MaxThreads / W, NY + 1);
+    if (W > maxt / 2 || own_x < std::min(NX, 15)) continue;
+    const int R = std::min(maxt / W, NY + 1);
     if (R < 2) continue;
     const int ty = (NY + R - 2) / (R - 1);
     const int tiles = T * ty;
@@ -326,12 +330,21 @@ void fine_apply_p64(const FineOp& op, const double* u, double* y, cudaStream_t s
   PkCoefD C;
   SG_REQUIRE(op.walsh_ok && pk64_params(op, C), "FP64 apply: element matrix lacks the Walsh block form");
   const GridDesc& g = op.grid.d;
-  const P64Plan pl = p64_plan(g, num_sms());
+  // 256-thread blocks, two CTAs per SM (32 warps; the FP64 dependency waits
+  // and per-layer barriers of one CTA overlap the other's work) at the price
+  // of a taller y halo: 35.6 -> 35.0 us at 100^3, 211.7 -> 204 us at 200^3,
+  // same bits (the owner sum order does not depend on the tiling).
+  // SG_P64_NT=512 restores one 512-thread CTA per SM (A/B switch, read once).
+  static const int nt_env = [] {
+    const char* e = std::getenv("SG_P64_NT");
+    return e && std::atoi(e) == 512 ? kP64MaxThreads : 256;
+  }();
+  const P64Plan pl = p64_plan(g, num_sms(), nt_env);
   SG_REQUIRE(pl.W > 0, "FP64 apply: no tiling for this grid");
-  // always a full 512-thread block (W * R <= 512; the extra threads only help
+  // always a full block (W * R <= block size; the extra threads only help
   // stage planes): the block size is then a compile-time constant of the
   // kernel (constant shared-memory offsets: 36.9 -> 35.3 us at 100^3)
-  const int threads = kP64MaxThreads;
+  const int threads = nt_env;
   const int SL = (pl.R + 1) * 3 * (pl.W + 1);
   const size_t smem = sizeof(double) * (2 * size_t(SL) + 18 * size_t(threads) +
                                         2 * size_t(pl.R - 1) * 3 * (pl.W - 1));
@@ -347,7 +360,9 @@ void fine_apply_p64(const FineOp& op, const double* u, double* y, cudaStream_t s
   };
   static const bool rt_nt = std::getenv("SG_P64_RTNT") != nullptr;
   static_assert(kP64MaxThreads == 512, "fine_p64_kernel<LD, 512> below");
-  if (ld <= 4 && !rt_nt) go(fine_p64_kernel<4, 512>);
+  if (threads == 256 && ld <= 4) go(fine_p64_kernel<4, 256>);
+  else if (threads == 256 && ld <= 8) go(fine_p64_kernel<8, 256>);
+  else if (ld <= 4 && !rt_nt) go(fine_p64_kernel<4, 512>);
   else if (ld <= 4) go(fine_p64_kernel<4, 0>);
   else if (ld <= 6) go(fine_p64_kernel<6, 0>);
   else go(fine_p64_kernel<8, 0>);

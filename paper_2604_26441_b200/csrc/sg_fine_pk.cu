@@ -106,15 +106,17 @@ __device__ __forceinline__ float2 ldp2(const float* p) {
 // a multiple of 32 floats), so every address is base + immediate and the
 // per-layer address arithmetic (IMAD on the FMA pipe) disappears; XSC = 0:
 // runtime stride (rows wider than 256 nodes).
-template <int MODE, int XSC>
-__global__ void __launch_bounds__(kPkMaxThreads, 1)
+// NT: block size (512: one CTA per SM, 16 warps; 256: two CTAs per SM, so one
+// CTA's per-layer barrier and epilogue overlap the other's transforms)
+template <int MODE, int XSC, int NT>
+__global__ void __launch_bounds__(NT, kPkMaxThreads / NT)
 fine_pk_kernel(GridDesc g, const uint8_t* __restrict__ nmask, const float* __restrict__ u,
                float* __restrict__ yout, const float* __restrict__ E, PkCoef C, int P, int R,
                int kchunk, int XS_, int SX, PkEpi ep) {
   const int XS = XSC > 0 ? XSC : XS_;
   // published partials [buf][q][thread]: q 0..2 = i0(row 0), 3..5 = i1(row 0),
   // 6..8 = i2(row 0), 9..11 = i2(row 1), 3 comps each
-  __shared__ float pub[2][12][kPkMaxThreads];
+  __shared__ float pub[2][12][NT];
   // PK_CHEB: this plane's b, dinv, x, d of the owned node pair, prefetched
   // with cp.async at the top of the layer ([q][thread], q = array*3 + comp)
   extern __shared__ float2 epre[];
@@ -227,7 +229,7 @@ fine_pk_kernel(GridDesc g, const uint8_t* __restrict__ nmask, const float* __res
 #pragma unroll
           for (int c = 0; c < 3; ++c) {
             const unsigned dst = static_cast<unsigned>(
-                __cvta_generic_to_shared(epre + (a * 3 + c) * kPkMaxThreads + t));
+                __cvta_generic_to_shared(epre + (a * 3 + c) * NT + t));
             const float* gp = src[a] + orow + oplane * pl + int64_t(c) * XS;
             asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(gp) : "memory");
           }
@@ -330,15 +332,15 @@ fine_pk_kernel(GridDesc g, const uint8_t* __restrict__ nmask, const float* __res
           if constexpr (MODE == PK_Y) {
             *reinterpret_cast<float2*>(yout + o) = make_float2(y0, y1);
           } else if constexpr (MODE == PK_CHEB) {
-            const float2 bb = epre[(0 + c) * kPkMaxThreads + t];
-            const float2 di = epre[(3 + c) * kPkMaxThreads + t];
-            const float2 xx = epre[(6 + c) * kPkMaxThreads + t];
+            const float2 bb = epre[(0 + c) * NT + t];
+            const float2 di = epre[(3 + c) * NT + t];
+            const float2 xx = epre[(6 + c) * NT + t];
             // scalar round-to-nearest intrinsics: never contracted (ptxas
             // was seen fusing even explicit mul.rn/add.rn .f32x2 into FFMA2)
             float2 dn = make_float2(__fmul_rn(ep.A, __fmul_rn(di.x, __fsub_rn(bb.x, y0))),
                                     __fmul_rn(ep.A, __fmul_rn(di.y, __fsub_rn(bb.y, y1))));
             if (!ep.first) {
-              const float2 dd = epre[(9 + c) * kPkMaxThreads + t];
+              const float2 dd = epre[(9 + c) * NT + t];
               dn.x = __fadd_rn(dn.x, __fmul_rn(ep.AC, dd.x));
               dn.y = __fadd_rn(dn.y, __fmul_rn(ep.AC, dd.y));
             }
@@ -492,8 +494,28 @@ bool p32_supported(const FineOp& op) {
 // overlapping by two pairs (stride SX = 2P - 4 nodes), P as small as T
 // allows; y: tiles of R element rows overlapping by one; z: chunks of kchunk
 // node planes (+ one recomputed layer) minimising waves x (chunk + 1).
-PkPlan pk_plan(const GridDesc& g, int nsm) {
+// Block size of the P32 kernels.  512 threads = one CTA (16 warps) per SM;
+// 256 = two CTAs per SM, each CTA's per-layer barrier and epilogue then
+// overlapping the other's transforms, at the price of a taller y halo (R - 1
+// of R rows owned).  Measured at 100^3 (bit-identical): the fused smoother
+// 33.6 -> 31.4 us and the fused residual 31.0 -> 30.0 us at 256, the plain
+// apply 22.3 -> 22.8 us; at 200^3 (R = 4 at 256) every mode is slower.  So
+// the fused modes run 256-thread blocks when that still leaves R >= 5 rows.
+// SG_PK_NT=256|512 forces one size for every mode (A/B switch, read once).
+int pk_threads(const GridDesc& g, int mode) {
+  static const int env = [] {
+    const char* e = getenv("SG_PK_NT");
+    const int v = e ? atoi(e) : 0;
+    return v == 256 || v == 512 ? v : 0;
+  }();
+  if (env) return env;
+  const int P = (g.nx + 2) / 2;
+  return mode != PK_Y && P <= 64 && 256 / P >= 5 ? 256 : kPkMaxThreads;
+}
+
+PkPlan pk_plan(const GridDesc& g, int nsm, int nt) {
   PkPlan pl;
+  nsm *= kPkMaxThreads / nt;  // resident CTAs per wave
   int P = (g.nx + 2) / 2, T = 1, SX = 2 * P;
   if (P > 64) {
     for (T = 2;; ++T) {
@@ -502,7 +524,7 @@ PkPlan pk_plan(const GridDesc& g, int nsm) {
     }
     SX = 2 * P - 4;
   }
-  int R = std::max(2, kPkMaxThreads / P);
+  int R = std::max(2, nt / P);
   R = std::min(R, g.ny + 2);
   const int tilesy = (g.ny + 1 + (R - 1) - 1) / (R - 1);
   const int planes = g.nz + 1;
@@ -519,6 +541,7 @@ PkPlan pk_plan(const GridDesc& g, int nsm) {
   const int kchunk = (planes + nch - 1) / nch;
   nch = (planes + kchunk - 1) / kchunk;
   pl.P = P; pl.T = T; pl.SX = SX; pl.R = R; pl.tilesy = tilesy; pl.kchunk = kchunk; pl.nch = nch;
+  pl.nt = nt;
   return pl;
 }
 
@@ -527,34 +550,40 @@ static void launch_pk(const FineOp& op, const float* u, float* y, const PkEpi& e
   PkCoef C;
   SG_REQUIRE(op.walsh_ok && pk_params(op, C), "P32 apply: element matrix lacks the Walsh block form");
   const GridDesc& g = op.grid.d;
-  const PkPlan pl = pk_plan(g, num_sms());
+  const PkPlan pl = pk_plan(g, num_sms(), pk_threads(g, MODE));
   const int P = pl.P, R = pl.R, SX = pl.SX, kchunk = pl.kchunk;
   const int threads = ((P * R + 31) / 32) * 32;
   dim3 grid(pl.T, pl.tilesy, pl.nch);
-  const size_t dyn = MODE == PK_CHEB ? sizeof(float2) * 12 * kPkMaxThreads : 0;
   const int XS = p32_xs(g);
-  static bool attr_set[9] = {};
-  auto go = [&](auto kern) {
+  static bool attr_set[2][9] = {};
+  auto go = [&](auto kern, auto ntc) {
+    constexpr int NT = decltype(ntc)::value;
+    const size_t dyn = MODE == PK_CHEB ? sizeof(float2) * 12 * NT : 0;
     const int slot = XS <= 256 && XS % 32 == 0 ? XS / 32 : 0;
-    if (MODE == PK_CHEB && !attr_set[slot]) {
+    if (MODE == PK_CHEB && !attr_set[NT == 256][slot]) {
       SG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(dyn)));
-      attr_set[slot] = true;
+      attr_set[NT == 256][slot] = true;
     }
     kern<<<grid, threads, dyn, s>>>(g, op.grid.nmask.p, u, y, op.E32.p, C, P, R, kchunk, XS, SX, ep);
   };
-  // (the fused Chebyshev variant keeps the runtime stride: with a constant one
-  // ptxas hoists more offsets and spills; measured slower)
-  switch (MODE == PK_CHEB ? 0 : XS) {
-    case 32: go(fine_pk_kernel<MODE, 32>); break;
-    case 64: go(fine_pk_kernel<MODE, 64>); break;
-    case 96: go(fine_pk_kernel<MODE, 96>); break;
-    case 128: go(fine_pk_kernel<MODE, 128>); break;
-    case 160: go(fine_pk_kernel<MODE, 160>); break;
-    case 192: go(fine_pk_kernel<MODE, 192>); break;
-    case 224: go(fine_pk_kernel<MODE, 224>); break;
-    case 256: go(fine_pk_kernel<MODE, 256>); break;
-    default: go(fine_pk_kernel<MODE, 0>); break;
-  }
+  auto by_xs = [&](auto ntc) {
+    constexpr int NT = decltype(ntc)::value;
+    // (the fused Chebyshev variant keeps the runtime stride: with a constant one
+    // ptxas hoists more offsets and spills; measured slower)
+    switch (MODE == PK_CHEB ? 0 : XS) {
+      case 32: go(fine_pk_kernel<MODE, 32, NT>, ntc); break;
+      case 64: go(fine_pk_kernel<MODE, 64, NT>, ntc); break;
+      case 96: go(fine_pk_kernel<MODE, 96, NT>, ntc); break;
+      case 128: go(fine_pk_kernel<MODE, 128, NT>, ntc); break;
+      case 160: go(fine_pk_kernel<MODE, 160, NT>, ntc); break;
+      case 192: go(fine_pk_kernel<MODE, 192, NT>, ntc); break;
+      case 224: go(fine_pk_kernel<MODE, 224, NT>, ntc); break;
+      case 256: go(fine_pk_kernel<MODE, 256, NT>, ntc); break;
+      default: go(fine_pk_kernel<MODE, 0, NT>, ntc); break;
+    }
+  };
+  if (pl.nt == 256) by_xs(std::integral_constant<int, 256>{});
+  else by_xs(std::integral_constant<int, 512>{});
   SG_CHECK_LAUNCH();
 }
 

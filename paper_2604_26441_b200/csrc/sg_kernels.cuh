@@ -49,8 +49,10 @@ int64_t p32_size(const GridDesc& g);
 bool p32_supported(const FineOp& op);
 struct PkPlan {
   int P = 0, T = 1, SX = 0, R = 0, tilesy = 0, kchunk = 0, nch = 0;
+  int nt = 512;  // block size
 };
-PkPlan pk_plan(const GridDesc& g, int nsm);
+PkPlan pk_plan(const GridDesc& g, int nsm, int nt);
+int pk_threads(const GridDesc& g, int mode);  // mode: 0 plain, 1 Chebyshev, 2 residual
 void fine_apply_p32(const FineOp& op, const float* u, float* y, cudaStream_t s);
 void fine_apply_p32_cheb(const FineOp& op, const float* x, float* xout, const float* b,
                          const float* dinv, float* d, float A, float AC, bool first, cudaStream_t s,

@@ -305,8 +305,9 @@ def test_fine_apply_fp64_block_tiling(dims, kind):
 
 
 def test_fine_apply_fp64_block_size_bit_identical():
-    """The FP64 apply with its compile-time 512-thread block size equals the
-    runtime-block-size instantiation (SG_P64_RTNT=1) bit for bit."""
+    """The FP64 apply's default 256-thread, two-CTAs-per-SM tiling equals the
+    512-thread tiling (SG_P64_NT=512) with a compile-time and with a runtime
+    block size (SG_P64_RTNT=1) bit for bit."""
     import os
     import subprocess
     import sys
@@ -321,12 +322,47 @@ def test_fine_apply_fp64_block_size_bit_identical():
         "    out[str(dims)] = op.matvec_tagged(P.SplitMix64(5).gaussian(g.n_free), P.PrecisionTag.FP64)\n"
         "np.savez(sys.argv[1], **out)\n" % root)
     res = {}
-    for name, env in (("ct", {}), ("rt", {"SG_P64_RTNT": "1"})):
+    for name, env in (("ct", {"SG_P64_NT": "512"}), ("rt", {"SG_P64_NT": "512", "SG_P64_RTNT": "1"}),
+                      ("nt256", {})):
         path = f"/tmp/_p64nt_{name}.npz"
         subprocess.run([sys.executable, "-c", code, path], check=True, env=dict(os.environ, **env))
         res[name] = np.load(path)
     for k in res["ct"].files:
         assert np.array_equal(res["ct"][k], res["rt"][k]), k
+        assert np.array_equal(res["ct"][k], res["nt256"][k]), k
+
+
+def test_p32_block_size_bit_identical():
+    """The level-0 P32 kernels with 512-thread blocks (one CTA per SM) and with
+    256-thread blocks (two per SM, a taller y halo) give the same bits: the
+    plain FP32 apply, and the V-cycle that runs the fused smoother / residual
+    applies (SG_PK_NT forces one block size for every mode)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = (
+        "import sys, warnings, numpy as np; sys.path.insert(0, %r)\n"
+        "import paper_2604_26441_b200 as P\n"
+        "out = {}\n"
+        "for dims, kind in (((100,100,100),'uniform'), ((64,48,40),'binary'), ((131,7,5),'random_floor')):\n"
+        "    g = P.build_cantilever(*dims)\n"
+        "    op = P.FineOperator(g, P.simp_modulus(P.make_state(kind, *dims, vf=0.5, seed=42), 3.0))\n"
+        "    u = P.SplitMix64(5).gaussian(g.n_free)\n"
+        "    out['a' + str(dims)] = op.matvec_tagged(u.astype(np.float32), P.PrecisionTag.FP32)\n"
+        "    with warnings.catch_warnings():\n"
+        "        warnings.simplefilter('ignore')\n"
+        "        h = P.build_hierarchy(op, 4, 'fp32')\n"
+        "    out['v' + str(dims)] = h.vcycle(u)\n"
+        "np.savez(sys.argv[1], **out)\n" % root)
+    res = {}
+    for nt in ("512", "256"):
+        path = f"/tmp/_p32nt_{nt}.npz"
+        subprocess.run([sys.executable, "-c", code, path], check=True,
+                       env=dict(os.environ, SG_PK_NT=nt))
+        res[nt] = np.load(path)
+    for k in res["512"].files:
+        assert np.array_equal(res["512"][k], res["256"][k]), k
 
 
 @pytest.mark.parametrize("dims,kind", [((100, 100, 100), "uniform"), ((131, 7, 5), "binary"),

@@ -19,9 +19,12 @@ def _brick(n, nsm=148):
     return tuple(out)
 
 
-def _p32(n, nsm=148):
+def _p32(n, nsm=148, nt=None):
     out = (ctypes.c_int32 * 7)()
-    _native.check(_native.load().sg_plan_p32(n[0], n[1], n[2], nsm, out))
+    if nt is None:
+        _native.check(_native.load().sg_plan_p32(n[0], n[1], n[2], nsm, out))
+    else:
+        _native.check(_native.load().sg_plan_p32_bs(n[0], n[1], n[2], nsm, nt, out))
     return dict(zip(("P", "T", "SX", "R", "tilesy", "kchunk", "nch"), out))
 
 
@@ -51,11 +54,12 @@ def test_brick_plan_100cube_coarsest():
 
 @pytest.mark.parametrize("dims", [(100, 100, 100), (200, 200, 200), (1, 1, 1), (9, 33, 17),
                                   (127, 4, 3), (131, 7, 5), (257, 2, 3), (40, 40, 40)])
-def test_p32_tiling_owns_every_node_once(dims):
+@pytest.mark.parametrize("nt", [None, 512, 256])
+def test_p32_tiling_owns_every_node_once(dims, nt):
     nx, ny, nz = dims
-    pl = _p32(dims)
+    pl = _p32(dims, nt=nt)
     P, T, SX, R = pl["P"], pl["T"], pl["SX"], pl["R"]
-    assert P <= 64 and P * R <= 512 and R >= 2
+    assert P <= 64 and P * R <= (nt or 512) and R >= 2
     # x: pair p of tile t covers elements xo+2p, xo+2p+1 and owns nodes in [own_lo, own_hi)
     xown = np.zeros(nx + 1, int)
     for t in range(T):
