@@ -330,8 +330,9 @@ void fine_apply_p64(const FineOp& op, const double* u, double* y, cudaStream_t s
   PkCoefD C;
   SG_REQUIRE(op.walsh_ok && pk64_params(op, C), "FP64 apply: element matrix lacks the Walsh block form");
   const GridDesc& g = op.grid.d;
-  // 256-thread blocks, two CTAs per SM (32 warps; the FP64 dependency waits
-  // and per-layer barriers of one CTA overlap the other's work) at the price
+  // 256-thread blocks, two independent CTAs per SM (still 16 warps at 128
+  // registers; one CTA's FP64 dependency waits and per-layer barrier overlap
+  // the other's work) at the price
   // of a taller y halo: 35.6 -> 35.0 us at 100^3, 211.7 -> 204 us at 200^3,
   // same bits (the owner sum order does not depend on the tiling).
   // SG_P64_NT=512 restores one 512-thread CTA per SM (A/B switch, read once).

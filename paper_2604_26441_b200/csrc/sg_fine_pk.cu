@@ -33,6 +33,14 @@ __device__ __forceinline__ float2 sub2(float2 a, float2 b) {
 }
 __device__ __forceinline__ float2 mul2(float2 a, float2 b) { return __fmul2_rn(a, b); }
 __device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) { return __ffma2_rn(a, b, c); }
+// A product that feeds an addition: two scalar mul.rn.f32.  ptxas contracts
+// mul.rn.f32x2 followed by add.rn.f32x2 into FFMA2 (the .rn does not stop it
+// for the packed forms), and it decides that per code copy: the same source
+// then rounded differently in an unrolled copy or another instantiation.
+// Scalar mul.rn is never contracted, so every rounding is the one written here.
+__device__ __forceinline__ float2 mul2s(float2 a, float2 b) {
+  return make_float2(__fmul_rn(a.x, b.x), __fmul_rn(a.y, b.y));
+}
 // x/y stage of one node plane for an element pair: raw[y][x][c] (x = node
 // columns ex, ex+1, ex+2; y = rows ej, ej+1) -> Q[c][m], m = mode in the xy
 // Walsh basis (0: const, 1: x, 2: y, 3: xy), lanes = (e0, e1).
@@ -216,6 +224,10 @@ fine_pk_kernel(GridDesc g, const uint8_t* __restrict__ nmask, const float* __res
   };
   float2 Eraw = load_E(k0 - 1);
 
+  // plain apply: two layers per trip, so the plane transforms alternate
+  // between Qlo and Qhi without register copies (safe for the bits because no
+  // product is contracted, mul2s above); the fused modes spill when unrolled
+#pragma unroll(MODE == PK_Y ? 2 : 1)
   for (int ek = k0 - 1; ek < k1; ++ek) {
     plane_q(Qhi);  // node plane ek+1
     advance(pk >= 0 && pk < g.nz);
@@ -259,9 +271,9 @@ fine_pk_kernel(GridDesc g, const uint8_t* __restrict__ nmask, const float* __res
       w[3] = fma2(kA, v[3], t1);
       w[7] = fma2(kA, v[7], t1);
       w[14] = fma2(kA, v[14], t1);
-      w[4] = w[6] = mul2(kC, add2(v[4], v[6]));
-      w[5] = w[12] = mul2(kC, add2(v[5], v[12]));
-      w[8] = w[13] = mul2(kC, add2(v[8], v[13]));
+      w[4] = w[6] = mul2s(kC, add2(v[4], v[6]));
+      w[5] = w[12] = mul2s(kC, add2(v[5], v[12]));
+      w[8] = w[13] = mul2s(kC, add2(v[8], v[13]));
       w[9] = fma2(kD, v[9], mul2(kE, v[20]));
       w[20] = fma2(kD, v[20], mul2(kE, v[9]));
       w[10] = fma2(kD, v[10], mul2(kE, v[17]));
@@ -272,9 +284,9 @@ fine_pk_kernel(GridDesc g, const uint8_t* __restrict__ nmask, const float* __res
       w[11] = fma2(kF, v[11], t2);
       w[16] = fma2(kF, v[16], t2);
       w[18] = fma2(kF, v[18], t2);
-      w[21] = mul2(kH, v[21]);
-      w[22] = mul2(kH, v[22]);
-      w[23] = mul2(kH, v[23]);
+      w[21] = mul2s(kH, v[21]);
+      w[22] = mul2s(kH, v[22]);
+      w[23] = mul2s(kH, v[23]);
     }
     // inverse z stage + the layer below's top half (same node plane ek)
     float2 T[3][4];
