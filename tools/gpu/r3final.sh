@@ -13,10 +13,8 @@ python tools/launch_summary.py gpurun_out/final_solve.csv > gpurun_out/final_sol
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/final_launches.csv \
     python bench.py --steps 2 --warmup 3 --no-cpu-baseline > /dev/null 2>&1
 python tools/launch_summary.py gpurun_out/final_launches.csv > gpurun_out/final_launches_summary.txt
-NCU="ncu --set full --clock-control none --import-source on --kernel-name-base demangled"
-for k in "fine_pk_kernel<1" "fine_pk_kernel<2" "fine_p64_kernel"; do
-  n=$(echo "$k" | tr -c 'a-z0-9_\n' '_')
-  $NCU --profile-from-start off -k "regex:$k" -c 1 -o gpurun_out/ncu/$n python tools/solve_launches.py 100 > /dev/null 2>&1
-done
+NCU="ncu --set full --clock-control none --import-source on"
+# the four level-0 applies (plain, fused smoother, fused residual, FP64) of tools/pk_kernels.py
+$NCU --profile-from-start off -k regex:fine_p -c 4 -o gpurun_out/ncu/fine_level0 python tools/pk_kernels.py 100 > gpurun_out/final_pk_ncu.log 2>&1
 for f in gpurun_out/ncu/*.ncu-rep; do python tools/ncu_summary.py $f; done > gpurun_out/final_ncu_summary.txt 2>&1
 rm -f gpurun_out/final_solve.csv
