@@ -340,12 +340,16 @@ void fine_apply_p64(const FineOp& op, const double* u, double* y, cudaStream_t s
     const char* e = std::getenv("SG_P64_NT");
     return e && std::atoi(e) == 512 ? kP64MaxThreads : 256;
   }();
-  const P64Plan pl = p64_plan(g, num_sms(), nt_env);
+  P64Plan pl = p64_plan(g, num_sms(), nt_env);
+  int threads = nt_env;
+  if (pl.W == 0 && threads == 256) {  // rows too long for 256-thread tiles (NX > ~2000)
+    threads = kP64MaxThreads;
+    pl = p64_plan(g, num_sms(), threads);
+  }
   SG_REQUIRE(pl.W > 0, "FP64 apply: no tiling for this grid");
   // always a full block (W * R <= block size; the extra threads only help
   // stage planes): the block size is then a compile-time constant of the
   // kernel (constant shared-memory offsets: 36.9 -> 35.3 us at 100^3)
-  const int threads = nt_env;
   const int SL = (pl.R + 1) * 3 * (pl.W + 1);
   const size_t smem = sizeof(double) * (2 * size_t(SL) + 18 * size_t(threads) +
                                         2 * size_t(pl.R - 1) * 3 * (pl.W - 1));

@@ -293,7 +293,8 @@ def test_fine_apply_fp32_packed_tiling(dims, kind):
 @pytest.mark.parametrize("dims,kind", [((100, 100, 100), "uniform"), ((131, 7, 5), "binary"),
                                        ((9, 33, 17), "random_floor"), ((1, 1, 1), "uniform"),
                                        ((2, 61, 3), "binary"), ((200, 3, 2), "binary"),
-                                       ((257, 2, 3), "random_floor"), ((63, 40, 9), "binary")])
+                                       ((257, 2, 3), "random_floor"), ((63, 40, 9), "binary"),
+                                       ((2100, 2, 1), "binary")])
 def test_fine_apply_fp64_block_tiling(dims, kind):
     """FP64 apply (block-form, plane-shared Walsh kernel, sg_fine_p64.cu) across
     tile shapes -- x tiles, odd sizes, one element -- and configs[3] at full size."""
