@@ -1,4 +1,4 @@
-# rz_pupd_z32: p update one thread per node (default) vs per DOF (SG_RZP_ELEM=1)
+# rz_pupd_z32 experiment (not kept, DESIGN 6b; SG_RZP_ELEM no longer exists): p update one thread per node vs per DOF
 O=gpurun_out/r3i.txt
 : > $O
 for rep in 1 2; do
